@@ -1,0 +1,30 @@
+"""Build the CPU oracle shared library (TEST INFRASTRUCTURE, see gdraa_oracle.h).
+
+gcc -std=c11 -O2 -ffp-contract=off -fno-fast-math: IEEE binary32, one rounding per
+operation, no FMA contraction (DESIGN.md "Readings" AMB-4).
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "gdraa_oracle.c")
+LIB = os.path.join(HERE, "liboracle.so")
+
+CFLAGS = ["-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+          "-Wall", "-Wextra", "-Werror"]
+
+
+def build(force: bool = False) -> str:
+    if (not force and os.path.exists(LIB)
+            and os.path.getmtime(LIB) >= max(os.path.getmtime(SRC),
+                                             os.path.getmtime(os.path.join(HERE, "gdraa_oracle.h")))):
+        return LIB
+    cmd = ["gcc", *CFLAGS, SRC, "-o", LIB + ".tmp"]
+    subprocess.run(cmd, check=True)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv))

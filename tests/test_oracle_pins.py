@@ -1,0 +1,327 @@
+"""Pins of the CPU oracle against things other than itself (CPU only).
+
+Each test names what fixes the expected value: a worked example printed in the paper /
+SPEC (tests/golden/spec_examples.json, cited per entry), exact rational arithmetic, a
+closed form, an invariant, or an independent library routine (torch's bf16 cast).
+"""
+import itertools
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests._exact import exact, f32_bits, fraction_to_f32
+
+F32 = np.float32
+
+
+# ---------------------------------------------------------------------------------------
+# Partition, Algorithm 1 "Divide D(i) by N", AMB-8
+# ---------------------------------------------------------------------------------------
+
+def test_partition_spec_examples(golden):
+    for ex in golden["partition_q1"]:
+        got = [oracle.partition(ex["L"], ex["N"], r, Q=1) for r in range(ex["N"])]
+        assert [list(b) for b in got] == ex["blocks"], ex["cite"]
+
+
+@pytest.mark.parametrize("Q", [1, 64])
+def test_partition_invariants(Q):
+    # blocks cover [0, L) exactly, sorted, disjoint; pure function.
+    rng = np.random.default_rng(0)
+    cases = [(L, N) for L in (1, 2, 3, 7, 63, 64, 65, 1000, 4096, 1 << 20, synth.L_R50,
+                              synth.L_R101) for N in range(1, 33)]
+    cases += [(int(rng.integers(1, 10**7)), int(rng.integers(1, 33))) for _ in range(200)]
+    for L, N in cases:
+        blocks = [oracle.partition(L, N, r, Q=Q) for r in range(N)]
+        assert blocks == [oracle.partition(L, N, r, Q=Q) for r in range(N)]
+        pos = 0
+        for off, ln in blocks:
+            assert off == pos
+            pos += ln
+        assert pos == L
+        blk = math.ceil(math.ceil(L / N) / Q) * Q
+        lens = [ln for _, ln in blocks]
+        # every block but the trailing (short / empty) ones is exactly one block length
+        full = [ln == blk for ln in lens]
+        k = full.index(False) if False in full else N
+        assert all(full[:k]) and all(ln < blk for ln in lens[k:])
+        assert all(lens[i] >= lens[i + 1] for i in range(N - 1))
+        assert all(off % Q == 0 or ln == 0 for off, ln in blocks)
+
+
+def test_partition_resnet_sizes():
+    # R50 N=8 -> 7 x 3,194,688 + 3,194,216; R101 N=8 -> 7 x 5,568,704
+    # + 5,568,232 (closed form: ceil(L/8) rounded up to 64, remainder in the last block).
+    r50 = [oracle.partition(synth.L_R50, 8, r)[1] for r in range(8)]
+    assert r50 == [3_194_688] * 7 + [3_194_216]
+    r101 = [oracle.partition(synth.L_R101, 8, r)[1] for r in range(8)]
+    assert r101 == [5_568_704] * 7 + [5_568_232]
+
+
+def test_partition_rejects():
+    for args in [(0, 2, 0), (10, 0, 0), (10, 33, 0), (10, 2, 2), (10, 2, -1)]:
+        with pytest.raises(ValueError):
+            oracle.partition(*args)
+
+
+# ---------------------------------------------------------------------------------------
+# bf16 conversions (AMB-13): pinned to torch's own bf16 cast (library routine).
+# ---------------------------------------------------------------------------------------
+
+def test_bf16_rne_ties_to_even():
+    assert oracle.f32_to_bf16_rne(1.0 + 2.0**-8) == 0x3F80          # tie -> even (1.0)
+    assert oracle.f32_to_bf16_rne(1.0 + 3 * 2.0**-8) == 0x3F82      # tie -> even (1.015625)
+    assert oracle.f32_to_bf16_rne(-0.0) == 0x8000
+
+
+def test_bf16_matches_torch():
+    rng = np.random.default_rng(1)
+    x = np.concatenate([rng.standard_normal(20000).astype(F32) * F32(10) ** rng.integers(
+        -30, 30, 20000).astype(F32),
+        rng.integers(-(1 << 24), 1 << 24, 20000).astype(F32),
+        np.array([0.0, -0.0, 1.0 + 2**-8, 1.0 + 3 * 2**-8, 65504.0], dtype=F32)])
+    x = x[np.isfinite(x)]
+    ref = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    got = np.array([oracle.f32_to_bf16_rne(float(v)) for v in x[:5000]], dtype=np.uint16)
+    assert np.array_equal(got, ref[:5000])
+    # widening is exact: compare with torch bf16 -> f32
+    bits = rng.integers(0, 1 << 16, 4000).astype(np.uint16)
+    bits = bits[((bits >> 7) & 0xFF) != 0xFF]                    # finite only (AMB-16)
+    wide = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).float().numpy()
+    got_w = np.array([oracle.bf16_to_f32(int(b)) for b in bits], dtype=F32)
+    assert np.array_equal(got_w.view(np.uint32), wide.view(np.uint32))
+
+
+# ---------------------------------------------------------------------------------------
+# Aggregation "Average D(k,i)" (Eq. 3)
+# ---------------------------------------------------------------------------------------
+
+def test_mean_spec_examples(golden):
+    for ex in golden["mean"]:
+        got = oracle.allreduce_mean([np.array(x, dtype=F32) for x in ex["inputs"]])
+        assert np.array_equal(got, np.array(ex["out"], dtype=F32)), ex["cite"]
+
+
+def test_mean_n1_identity_bits():
+    # S:179 N=1 -> output = input, including the sign of zero and subnormals.
+    x = np.array([-0.0, 0.0, 1e-45, -3.5, 7e30], dtype=F32)
+    assert np.array_equal(oracle.allreduce_mean([x]).view(np.uint32), x.view(np.uint32))
+
+
+VALUES = [-2.0, -1.0, -0.5, -0.0, 0.0, 0.5, 1.0, 3.0]
+
+
+def _exact_expected(cols, N):
+    """Exact rational mean, rounded once; sign of an exact zero per IEEE RN rules for a
+    left fold: -0.0 iff every addend is -0.0."""
+    s = sum(exact(c) for c in cols)
+    m = fraction_to_f32(s / N)
+    if s == 0:
+        allneg = all(np.signbit(F32(c)) for c in cols)
+        return F32(-0.0) if allneg else F32(0.0)
+    return m
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4])
+def test_mean_bruteforce_exact(N):
+    # Brute force over a tiny value set: every partial sum of these dyadics is exact in
+    # fp32, so the only rounding is the single division (exact result rounded once).
+    cols = list(itertools.product(VALUES, repeat=N))
+    L = len(cols)
+    bufs = [np.array([c[p] for c in cols], dtype=F32) for p in range(N)]
+    got = oracle.allreduce_mean(bufs)
+    exp = np.array([_exact_expected(c, N) for c in cols], dtype=F32)
+    assert got.shape == (L,)
+    assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
+
+
+def test_mean_rank_order_pinned():
+    # AMB-2: a left fold in ascending rank starting at rank 0.  With x = [1, 2^-24,
+    # 2^-24, 2^-24]: 1 + 2^-24 ties to even -> 1 at every step, mean = 1/4 exactly.
+    # Any other order (e.g. right-to-left: 3*2^-24 + 1 -> 1 + 2^-22) gives 1/4 + 2^-24.
+    x = [np.array([v], dtype=F32) for v in (1.0, 2.0**-24, 2.0**-24, 2.0**-24)]
+    assert f32_bits(oracle.allreduce_mean(x)[0]) == f32_bits(0.25)
+    rev = x[::-1]
+    assert f32_bits(oracle.allreduce_mean(rev)[0]) == f32_bits(0.25 + 2.0**-24)
+
+
+def test_mean_division_not_reciprocal():
+    # AMB-2: one IEEE division by N (not multiplication by fl(1/N)).  For N = 3 and
+    # s = 3 * 5 = 15 ... pick s where fl(s/3) != fl(s * fl(1/3)): exact rounding decides.
+    N = 3
+    found = 0
+    for k in range(1, 2000):
+        s = F32(k) * F32(1.0 + 2.0**-20)
+        exp = fraction_to_f32(exact(s) / N)
+        recip = fraction_to_f32(exact(s) * exact(fraction_to_f32(Fraction(1, 3))))
+        if exp != recip:
+            found += 1
+            got = oracle.allreduce_mean([np.array([s], F32), np.array([0.0], F32),
+                                         np.array([0.0], F32)])[0]
+            assert f32_bits(got) == f32_bits(exp)
+    assert found > 10
+
+
+@pytest.mark.parametrize("N", [2, 3, 5, 7, 8, 16, 32])
+def test_mean_within_error_bound(N):
+    # Exact mean by rational arithmetic; the fp32 left fold + division must lie within
+    # the standard bound |m^ - m| <= (gamma_{N-1} sum|x| + u(|s| + gamma sum|x|)) / N.
+    L = 257
+    bufs = [synth.grad_like(7, p, L) for p in range(N)]
+    got = oracle.allreduce_mean(bufs)
+    u = Fraction(1, 2**24)
+    gamma = (N - 1) * u / (1 - (N - 1) * u)
+    for i in range(L):
+        xs = [exact(b[i]) for b in bufs]
+        s = sum(xs)
+        a = sum(abs(x) for x in xs)
+        bound = (gamma * a + u * (abs(s) + gamma * a)) / N
+        assert abs(exact(got[i]) - s / N) <= bound, i
+    # and against torch's float64 mean (library routine), same bound in float
+    ref = torch.from_numpy(np.stack(bufs)).double().mean(0).numpy()
+    assert np.allclose(got, ref, rtol=0, atol=float(N * 2.0**-22) * np.abs(np.stack(bufs)).max())
+
+
+@pytest.mark.parametrize("N", list(range(1, 33)))
+def test_mean_of_constant(N):
+    # "the mean of a constant is that constant" / "sum of N identical inputs = N x"
+    # (north star), with the precondition that x has <= 24 - ceil(log2 N) significant bits
+    # so that every partial sum k*x is exact (SURVEY.md §8(c) O3/O4 pin).
+    bits = 24 - math.ceil(math.log2(N)) if N > 1 else 24
+    rng = np.random.default_rng(N)
+    mant = rng.integers(1 << (bits - 1), 1 << bits, 500)
+    x = (mant * 2.0 ** rng.integers(-60, 20, 500).astype(np.float64)
+         * rng.choice([-1, 1], 500)).astype(F32)
+    got = oracle.allreduce_mean([x] * N)
+    assert np.array_equal(got.view(np.uint32), x.view(np.uint32))
+
+
+# ---------------------------------------------------------------------------------------
+# Update "Update model with gradient of differential D", AMB-4
+# ---------------------------------------------------------------------------------------
+
+def _one(v):
+    return np.array([v], dtype=F32)
+
+
+def test_sgd_spec_single_step(golden):
+    ex = golden["sgd"][0]
+    w, v = oracle.sgd_step([_one(ex["g"])], _one(ex["w"]), _one(0.0), ex["lr"], ex["mom"])
+    assert abs(float(w[0]) - ex["w_out"]) <= 2.0**-24 * 2, ex["cite"]
+    # exact: w' = RNE(1 - RNE(lr*1)) -- one rounding per operation (AMB-4)
+    lr = F32(ex["lr"])
+    assert f32_bits(w[0]) == f32_bits(fraction_to_f32(1 - exact(lr)))
+
+
+def test_sgd_spec_two_steps(golden):
+    ex = golden["sgd"][1]
+    w, v = _one(ex["w"]), _one(0.0)
+    ws = [float(w[0])]
+    for _ in range(ex["steps"]):
+        w, v = oracle.sgd_step([_one(ex["g"])] * 4, w, v, ex["lr"], ex["mom"])
+        ws.append(float(w[0]))
+    dec = [ws[k] - ws[k + 1] for k in range(ex["steps"])]
+    assert np.allclose(dec, ex["decreases"], rtol=0, atol=1e-6), ex["cite"]
+
+
+def test_sgd_dyadic_closed_form():
+    # mu = 1/2, lr = 1/4, g = 1 on every rank, w0 = 1, v0 = 0: every value is dyadic, so
+    # the closed form v_k = (1 - mu^k)/(1 - mu), w_k = w0 - lr * sum_j v_j holds exactly.
+    mu, lr = Fraction(1, 2), Fraction(1, 4)
+    for N in (1, 2, 3, 4, 8):
+        w, v = _one(1.0), _one(0.0)
+        wk = Fraction(1)
+        for k in range(1, 12):
+            w, v = oracle.sgd_step([_one(1.0)] * N, w, v, float(lr), float(mu))
+            vk = (1 - mu**k) / (1 - mu)
+            wk = wk - lr * vk
+            assert exact(v[0]) == vk and exact(w[0]) == wk, (N, k)
+
+
+@pytest.mark.parametrize("N", [1, 2, 4, 8])
+@pytest.mark.parametrize("bf16", [False, True])
+def test_sgd_integer_family_exact(N, bf16):
+    # Integer family (north star: "integer-valued test gradients must match bit-exactly"):
+    # with N a power of two every intermediate is exactly representable, so the result is
+    # the exact rational update.  Computed here with Fractions, checked representable.
+    L = 3000
+    gs = [synth.grad_integer(3, p, L, bf16=bf16) for p in range(N)]
+    w0, v0 = synth.w_integer(3, L), synth.v_integer(3, L)
+    lr, mom = synth.INT_LR, synth.INT_MOM
+    gin = [synth.to_bf16_bits_trunc(g) for g in gs] if bf16 else gs
+    w, v = oracle.sgd_step(gin, w0, v0, lr, mom)
+    for i in range(0, L, 7):
+        m = sum(exact(g[i]) for g in gs) / N
+        vn = Fraction(mom) * exact(v0[i]) + m
+        wn = exact(w0[i]) - Fraction(lr) * vn
+        assert exact(fraction_to_f32(vn)) == vn and exact(fraction_to_f32(wn)) == wn
+        assert exact(v[i]) == vn and exact(w[i]) == wn, i
+
+
+def test_sgd_signed_zero():
+    # AMB-3 + IEEE: all ranks -0.0 -> mean -0.0; v' = fl(fl(mu * (+0)) + (-0)) = +0.0,
+    # and with v = -0.0: fl(mu * -0) = -0, -0 + -0 = -0.
+    g = [_one(-0.0)] * 3
+    w, v = oracle.sgd_step(g, _one(1.0), _one(0.0), 0.1, 0.9)
+    assert f32_bits(v[0]) == f32_bits(0.0) and w[0] == F32(1.0)
+    w, v = oracle.sgd_step(g, _one(1.0), _one(-0.0), 0.1, 0.9)
+    assert f32_bits(v[0]) == f32_bits(-0.0)
+    assert f32_bits(oracle.allreduce_mean(g)[0]) == f32_bits(-0.0)
+
+
+def test_sgd_unfused_rounding():
+    # AMB-4: four separately rounded operations; find elements where fma(mu, v, m) would
+    # differ and check the oracle matches the exact per-operation rounding instead.
+    rng = np.random.default_rng(5)
+    L = 2000
+    g = [rng.standard_normal(L).astype(F32) for _ in range(2)]
+    w0 = rng.standard_normal(L).astype(F32)
+    v0 = rng.standard_normal(L).astype(F32)
+    lr, mom = F32(0.1), F32(0.9)
+    w, v = oracle.sgd_step(g, w0, v0, lr, mom)
+    diff_fma = 0
+    for i in range(L):
+        s = fraction_to_f32(exact(g[0][i]) + exact(g[1][i]))
+        m = fraction_to_f32(exact(s) / 2)
+        t = fraction_to_f32(exact(mom) * exact(v0[i]))
+        vn = fraction_to_f32(exact(t) + exact(m))
+        u = fraction_to_f32(exact(lr) * exact(vn))
+        wn = fraction_to_f32(exact(w0[i]) - exact(u))
+        assert f32_bits(v[i]) == f32_bits(vn) and f32_bits(w[i]) == f32_bits(wn), i
+        if fraction_to_f32(exact(mom) * exact(v0[i]) + exact(m)) != vn:
+            diff_fma += 1
+    assert diff_fma > 0          # the test distinguishes fused from unfused
+
+
+# ---------------------------------------------------------------------------------------
+# Lemma 1 / Lemma 2 counters
+# ---------------------------------------------------------------------------------------
+
+def test_counters_lemmas(golden):
+    ex = golden["lemma1_bytes"][0]
+    for r in range(ex["N"]):
+        c = oracle.counters(ex["L"], ex["N"], r, ex["width"], ex["width"], Q=1)
+        assert c["rs_sent"] == c["rs_recv"] == c["ag_sent"] == c["ag_recv"] \
+            == ex["bytes_per_phase"], ex["cite"]
+        assert c["sync_waits"] == 2
+    ex = golden["lemma2_ops"][0]
+    c = oracle.counters(ex["L"], ex["N"], 0, 4, 4, Q=1)
+    assert (c["adds"], c["divides"], c["adds"] + c["divides"]) == \
+        (ex["adds"], ex["muls"], ex["total"]), ex["cite"]
+
+
+@pytest.mark.parametrize("L,N", [(1000, 8), (7, 3), (3, 4), (synth.L_R50, 8), (1, 1),
+                                 (synth.L_R101, 5)])
+def test_counters_conservation(L, N):
+    cs = [oracle.counters(L, N, r, 2, 4) for r in range(N)]
+    # every byte sent is received (reduce and broadcast), and Eq. 4's Op = L per worker
+    # sums to N * L over the ring of owners.
+    assert sum(c["rs_sent"] for c in cs) == sum(c["rs_recv"] for c in cs)
+    assert sum(c["ag_sent"] for c in cs) == sum(c["ag_recv"] for c in cs)
+    assert sum(c["adds"] + c["divides"] for c in cs) == N * L
+    assert all(c["sync_waits"] == (2 if N > 1 else 0) for c in cs)
