@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark of the GDRAA hot path: the fused gradient allreduce + momentum-SGD step
+(gdraa_sgd_step) on ResNet-sized gradient buffers, 1 process per B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config r50|r101|r50bf16|c1]
+                    [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+One "step" = one gdraa_sgd_step over the whole gradient buffer (= one kernel launch:
+reduce -> average -> update -> broadcast, two device synchronisations).  Prints ONE JSON
+line on rank 0 (contract in DESIGN.md "Measurement").  Metric (BASELINE.json): bus GB/s
+of the fused allreduce+SGD and its fraction of the NVLink roofline; N = 1 has no NVLink
+traffic and reports the kernel's algorithmic HBM GB/s against the measured HBM copy peak.
+"""
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "allreduce+SGD bus GB/s and % NVLink roofline at 1/2/4/8 B200 (ResNet-50 grads)"
+CONFIGS = {
+    # name: (L, g dtype, description)
+    "c1": (synth.L_C1, "f32", "config 1: 1M-element fp32 gradient"),
+    "r50": (synth.L_R50, "f32", "config 2: ResNet-50 fp32 gradient buffer (25,557,032)"),
+    "r101": (synth.L_R101, "f32", "config 3: ResNet-101 fp32 gradient buffer (44,549,160)"),
+    "r50bf16": (synth.L_R50, "bf16", "config 4: ResNet-50 bf16 gradients, fp32 master w/v"),
+}
+NVLINK_NOMINAL_GBS = 900.0     # NVLink 5, per direction per GPU
+NVLINK_MEASURED_GBS = 770.0    # B200_PROFILING.md: measured peer copy per direction
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes(L, N, s_g, shard_lens):
+    """Per-rank algorithmic bytes of one step.
+    N = 1: HBM bytes of the local fused SGD, (s_g + 16) * L (read g, w, v; write w, v).
+    N >= 2: NVLink bus bytes per rank per direction, B_nv = (N-1)/N * L * (s_g + 4)
+    (reduce ingress of g + broadcast ingress of w; NCCL busBW convention)."""
+    if N == 1:
+        return (s_g + 16) * L
+    return (N - 1) / N * L * (s_g + 4)
+
+
+# ---------------------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# ---------------------------------------------------------------------------------------
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, torch_dev):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            import torch
+            uuid = str(torch.cuda.get_device_properties(torch_dev).uuid)
+            try:
+                self.h = pynvml.nvmlDeviceGetHandleByUUID("GPU-" + uuid)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(torch_dev)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:   # noqa: BLE001
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            self.sample()
+            self._stop.wait(0.005)
+
+    def sample(self):
+        if not self.ok:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in REASONS.items():
+                if mask & bit:
+                    self.reasons.add(name)
+        except Exception:   # noqa: BLE001
+            pass
+
+    def start(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def stop(self):
+        self._stop.set()
+        self.t.join()
+        self.sample()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons - {"gpu_idle"}),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------------
+# the oracle as a CPU baseline (rank 0 only)
+# ---------------------------------------------------------------------------------------
+def oracle_sample_step(L, N, g_dt, budget_s):
+    """Time the CPU oracle (single-threaded C, as it stands) on a bounded sample of the
+    workload: the first n elements of every rank's buffer, n sized to ~budget_s total.
+    Returns (bytes/s in the metric's definition, sample description, seconds)."""
+    import oracle
+    n = min(L, 1 << 20)
+    gs = [synth.grad_like(0, p, n) for p in range(N)]
+    if g_dt == "bf16":
+        gs = [synth.to_bf16_bits_trunc(g) for g in gs]
+    w, v = synth.w_like(0, n), np.zeros(n, np.float32)
+    s_g = 2 if g_dt == "bf16" else 4
+    t0 = time.perf_counter()
+    oracle.sgd_step(gs, w, v, synth.PAPER_LR, synth.PAPER_MOM)
+    t1 = time.perf_counter() - t0
+    reps = max(1, int(budget_s / max(t1, 1e-6)))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        w, v = oracle.sgd_step(gs, w, v, synth.PAPER_LR, synth.PAPER_MOM)
+    dt = (time.perf_counter() - t0) / reps
+    shard = [(n + N - 1) // N] * N
+    b = algorithmic_bytes(n, N, s_g, shard) * (N if N > 1 else 1)
+    return b / dt, (f"{reps} oracle steps over the first {n} elements of each of the {N} "
+                    f"rank buffers (of L={L})"), dt
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the same config and metric."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    L, g_dt, desc = CONFIGS[args.config]
+    N = args.gpus
+    s_g = 2 if g_dt == "bf16" else 4
+    budget = 60.0 / max(1, args.steps + args.warmup)   # whole run within ~1 minute
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, sample, dt = oracle_sample_step(L, N, g_dt, budget)
+        if i >= args.warmup:
+            vals.append((v, dt))
+    value = float(np.mean([v for v, _ in vals])) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": float(np.mean([d for _, d in vals])) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": config_dict(args, L, g_dt, desc, N),
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args, L, g_dt, desc, N):
+    return {"workload": args.config, "description": desc, "L": L, "g_dtype": g_dt,
+            "w_dtype": "f32", "v_dtype": "f32", "lr": synth.PAPER_LR, "mom": synth.PAPER_MOM,
+            "parallelism": f"dp{N}", "buffer_sets": args.sets,
+            "l2": f"inputs larger than L2: {args.sets} rotating (g, w, v) sets per rank"}
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="r50", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sets", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1802_02326_b200 import gdraa, jobserver
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    js = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        js = jobserver.setup_for_rank(world, rank, local)
+    gdraa.gdraa_init(world, rank)
+
+    L, g_dt, desc = CONFIGS[args.config]
+    N = world
+    s_g = 2 if g_dt == "bf16" else 4
+    tdt = torch.bfloat16 if g_dt == "bf16" else torch.float32
+    off, ln = gdraa.gdraa_shard(N, rank, L)
+
+    # synthetic inputs (host), then resident in HBM; S rotating sets so that no step
+    # finds its inputs in the 126 MB L2.
+    sets = []
+    for s in range(args.sets):
+        g_h = synth.grad_like(100 + s, rank, L)
+        if g_dt == "bf16":
+            g_h = synth.to_bf16_bits_trunc(g_h).view(np.int16)
+        g = torch.from_numpy(g_h).to(dev)
+        g = g.view(tdt) if g_dt == "bf16" else g
+        w = torch.from_numpy(synth.w_like(100 + s, L)).to(dev)
+        v = torch.zeros(L, dtype=torch.float32, device=dev)
+        gdraa.gdraa_register(w)
+        gdraa.gdraa_register(g)
+        sets.append((w, g, v))
+    lr, mom = synth.PAPER_LR, synth.PAPER_MOM
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    for k in range(args.warmup):
+        w, g, v = sets[k % len(sets)]
+        gdraa.gdraa_sgd_step(w, g, v, lr, mom, stream)
+    barrier()
+
+    st0 = gdraa.gdraa_get_stats()
+    clocks = ClockSampler(local) if rank == 0 else None
+    barrier()
+    if clocks:
+        clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for k in range(args.steps):
+        w, g, v = sets[k % len(sets)]
+        gdraa.gdraa_sgd_step(w, g, v, lr, mom, stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    barrier()
+    st1 = gdraa.gdraa_get_stats()
+    launches = st1["launches"] - st0["launches"]
+    ms_step = ms / args.steps
+    per_rank = algorithmic_bytes(L, N, s_g, None)
+    value = per_rank * N / (ms_step * 1e-3) / 1e9           # whole job
+    achieved = per_rank / (ms_step * 1e-3) / 1e9            # per rank = per launch
+
+    # ---- e2e: host buffers through the public API, copies inside the timed region ----
+    g_host = torch.empty(L, dtype=tdt, pin_memory=True)
+    g_host.copy_(sets[0][1].cpu())
+    w_out = torch.empty(ln, dtype=torch.float32, pin_memory=True)
+    w, g, v = sets[0]
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(args.e2e_steps):
+        g.copy_(g_host, non_blocking=True)
+        gdraa.gdraa_sgd_step(w, g, v, lr, mom, stream)
+        w_out.copy_(w[off:off + ln], non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ems], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e_val = per_rank * N / (ems / args.e2e_steps * 1e-3) / 1e9
+
+    # ---- NCCL all_reduce(AVG) of the same gradient buffer (reference point) ----
+    nccl = None
+    if world > 1 and not args.no_nccl:
+        buf = sets[0][1].clone()
+        for _ in range(5):
+            dist.all_reduce(buf, op=dist.ReduceOp.AVG)
+        barrier()
+        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0.record(stream)
+        for _ in range(20):
+            dist.all_reduce(buf, op=dist.ReduceOp.AVG)
+        n1.record(stream)
+        torch.cuda.synchronize()
+        nms = n0.elapsed_time(n1) / 20
+        t = torch.tensor([nms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        nms = float(t.item())
+        nccl = {"op": "torch.distributed.all_reduce(AVG)", "bytes": L * s_g,
+                "ms": nms, "bus_gbs_per_rank": 2 * (N - 1) / N * L * s_g / (nms * 1e-3) / 1e9,
+                "nccl": ".".join(map(str, torch.cuda.nccl.version()))}
+
+    if rank == 0:
+        peaks, peak_src = measured_peaks()
+        if N == 1:
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                    "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src,
+                    "bytes_per_launch": per_rank, "bytes_per_element": s_g + 16}
+        else:
+            roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_MEASURED_GBS,
+                    "unit": "GB/s", "frac": achieved / NVLINK_MEASURED_GBS,
+                    "peak_source": "measured B200 peer copy per direction (B200_PROFILING.md)",
+                    "frac_of_nominal_900": achieved / NVLINK_NOMINAL_GBS,
+                    "bytes_per_launch": per_rank}
+        roof["traffic"] = ncu_traffic(args.config, N)
+        roof["kernel_ms"] = ms_step
+        cpu = None
+        if N == 1 and not args.no_cpu_baseline:
+            cv, sample, _ = oracle_sample_step(L, N, g_dt, 10.0)
+            cpu = {"value": cv / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                   "sample": sample}
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": config_dict(args, L, g_dt, desc, N),
+            "value_definition": ("sum over ranks of per-rank algorithmic bytes / step time; "
+                                 + ("N=1: HBM bytes (s_g+16)*L" if N == 1 else
+                                    "N>=2: NVLink bus bytes (N-1)/N*L*(s_g+4) per rank")),
+            "bus_gbs_per_rank": achieved if N > 1 else 0.0,
+            "roofline": roof, "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "GB/s", "steps": args.e2e_steps,
+                    "h2d_bytes_per_step": L * s_g * N, "d2h_bytes_per_step": L * 4,
+                    "note": "all ranks: H2D of each rank's gradient from pinned host memory, "
+                            "gdraa_sgd_step, D2H of each rank's updated w shard"},
+            "gpu_launches": launches, "clocks": clocks.summary() if clocks else None,
+            "nccl_reference": nccl,
+        }
+        print(json.dumps(line), flush=True)
+
+    barrier()
+    gdraa.gdraa_finalize()
+    if js is not None:
+        js.communicate(timeout=60)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def ncu_traffic(config, N):
+    """dram bytes per launch from the committed ncu --set full summary, if one matches."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            tab = json.load(f)
+        return tab.get(f"{config}_n{N}")
+    except OSError:
+        return None
+
+
+if __name__ == "__main__":
+    sys.exit(main())

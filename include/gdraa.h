@@ -1,0 +1,189 @@
+/*
+ * gdraa.h -- C ABI of the B200-native GDRAA hot path (arxiv 1802.02326).
+ *
+ * GDRAA = "GPUDirect RDMA-Aware AllReduce" (PAPER.md = P:<line>; Algorithm 1
+ * P:142-174, §3).  Per training iteration every rank's gradient D(i) is
+ * divided into N blocks, block m of every rank is reduced and averaged by
+ * rank m ("Reduce" + "Aggregation"), the averaged block is applied to the
+ * weights and sent to every rank ("Broadcast"), with exactly two
+ * synchronisations per iteration (Alg. 1 lines 153/166).
+ *
+ * On one NVSwitch node the "registered memory region" of P:123 (ibv_reg_mr) becomes a
+ * CUDA IPC mapping of the caller's buffer in every peer process, and one sm_100a
+ * kernel per call pulls the owner shard from every peer over NVLink, sums it in rank
+ * order, divides by N, applies the momentum-SGD update, and pushes the updated shard
+ * into every peer's buffer.  A host job server only
+ * exchanges the 64-byte IPC handles and per-iteration go/done flags; it never touches
+ * weight data.
+ *
+ * Conventions for every entry point:
+ *  - Returns GDRAA_OK (0) or a negative gdraa_err_t.  On error a thread-local message
+ *    is available from gdraa_last_error().  Nothing is enqueued on an error return.
+ *  - Pointers named "device" are CUDA device pointers on the current device (the
+ *    device current at gdraa_init); "host" pointers are ordinary host memory.
+ *  - Calls that take a stream enqueue asynchronously and return immediately; results
+ *    are visible to later work on that stream.  Device-side failures (a peer that
+ *    never arrives within GDRAA_TIMEOUT_MS, default 30000) are STICKY: the next call and
+ *    gdraa_finalize return GDRAA_ETIMEOUT and gdraa_last_error() names the missing ranks.
+ *  - Collective calls (init, register, allreduce_mean, sgd_step, finalize) must be
+ *    issued in the same order with the same sizes on every rank, one outstanding
+ *    collective per process ("same iteration number and same L").
+ *  - The caller owns every data buffer and keeps it allocated until gdraa_finalize.
+ *    The library owns its signal pads, peer mappings and host-mapped flag pages.
+ */
+#ifndef GDRAA_H
+#define GDRAA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* A cudaStream_t (layout-compatible; NULL = the legacy default stream). */
+typedef struct CUstream_st *gdraa_stream_t;
+
+typedef enum { GDRAA_F32 = 0, GDRAA_BF16 = 1 } gdraa_dtype_t;
+
+typedef enum {
+    GDRAA_OK = 0,
+    GDRAA_EINVAL = -1,      /* bad argument (range, alignment, non-finite lr/mom, ...)   */
+    GDRAA_ENOTREG = -2,     /* buffer not registered with gdraa_register                   */
+    GDRAA_ESHAPE = -3,      /* n / dtype differ across ranks ("shape-mismatch")     */
+    GDRAA_ECUDA = -4,       /* a CUDA runtime/driver call failed                           */
+    GDRAA_ETIMEOUT = -5,    /* a peer missed a synchronisation ("peer-timeout")      */
+    GDRAA_ESTATE = -6,      /* not initialised / already initialised / after a fatal error */
+    GDRAA_EJOBSERVER = -7   /* job server unreachable or protocol error                    */
+} gdraa_err_t;
+
+/* Largest world on one NVSwitch node (the paper's design bound is 32 workers). */
+#define GDRAA_MAX_WORLD 8
+/* Shard alignment quantum in elements (AMB-8): shard starts are 64-element aligned. */
+#define GDRAA_SHARD_QUANTUM 64
+
+/*
+ * gdraa_init -- join the communicator (collective over all `world` ranks).
+ *   world: 1..GDRAA_MAX_WORLD ranks, one process per GPU of one node.
+ *   rank:  0..world-1 (SPEC 0-based ranks).
+ * Uses the CUDA device current on the calling thread.  For world > 1 the job server
+ * socket path is read from the environment variable GDRAA_JOBSERVER (started by
+ * paper_1802_02326_b200.jobserver); the call blocks until all ranks have joined and the
+ * signal pads are mapped (GDRAA_CONNECT_TIMEOUT_MS, default 120000).
+ * Errors: EINVAL (range), ESTATE (already initialised), EJOBSERVER, ECUDA.
+ */
+int gdraa_init(int world, int rank);
+
+/*
+ * gdraa_register -- register a device buffer for peer access (collective, P:123's
+ * "whole and continuous GPU memory registered by ibv_reg_mr").
+ *   buf:   device pointer, 16-byte aligned, n elements of dtype.  May point into a
+ *          larger cudaMalloc allocation (e.g. a PyTorch caching-allocator block); the
+ *          whole enclosing allocation is exported with cudaIpcGetMemHandle.
+ *   n:     element count >= 1, identical on every rank.
+ *   dtype: GDRAA_F32 or GDRAA_BF16, identical on every rank.
+ * Every rank must register its buffers in the same order.  Both the gradient g and
+ * the weights w of gdraa_sgd_step, and the buffer of gdraa_allreduce_mean, must be
+ * registered; the momentum buffer v is rank-local and need not be.
+ * Errors: EINVAL, ESTATE, ESHAPE (n/dtype mismatch across ranks, reported on every
+ * rank), EJOBSERVER, ECUDA.
+ */
+int gdraa_register(void *buf, size_t n, int dtype);
+
+/*
+ * gdraa_deregister -- forget a registration (local, not collective).  Peer mappings
+ * of the enclosing allocation stay open until gdraa_finalize, so the same memory can be
+ * registered again (e.g. after a caching allocator hands the address out anew).
+ *   buf: a pointer previously passed to gdraa_register.
+ * Errors: ENOTREG, ESTATE.
+ */
+int gdraa_deregister(void *buf);
+
+/*
+ * gdraa_allreduce_mean -- in place, buf <- (1/N) * sum_p buf_p on every rank
+ * (Algorithm 1 without the update).
+ *   buf: a registered device buffer (f32 or bf16).
+ *   s:   stream; the call is ordered after prior work on s on this rank.
+ * Per element: s = x_0; s = fl(s + x_p) for p = 1..N-1 (ascending rank); m = fl(s / N);
+ * bf16 buffers accumulate in fp32 and store bf16 RNE(m).  Bitwise deterministic and
+ * identical on every rank.  One kernel launch; two device-side synchronisations.
+ * Errors: ENOTREG, ESTATE, ETIMEOUT (sticky, from an earlier call), ECUDA.
+ */
+int gdraa_allreduce_mean(void *buf, gdraa_stream_t s);
+
+/*
+ * gdraa_sgd_step -- fused reduce -> average -> momentum-SGD update -> broadcast
+ * (Algorithm 1, hyper-parameters P:246).
+ *   w:   registered f32 device buffer, n elements, identical on all ranks before the
+ *        call; identical (updated) on all ranks after it.
+ *   g:   registered gradient buffer (f32 or bf16), n elements.  Read only.
+ *   v:   f32 device buffer, n elements, rank-local momentum state.  Only the owner
+ *        shard [off_r, off_r + len_r) of gdraa_shard() is read and written.
+ *   lr, mom: finite learning rate and momentum.
+ * Per element: m as in gdraa_allreduce_mean; v = fl(fl(mom*v) + m); w = fl(w - fl(lr*v))
+ * (four roundings, no FMA contraction).  Weight decay is not applied here.
+ * Errors: EINVAL, ENOTREG, ESTATE, ETIMEOUT (sticky), ECUDA.
+ */
+int gdraa_sgd_step(float *w, const void *g, float *v, float lr, float mom, gdraa_stream_t s);
+
+/*
+ * gdraa_shard -- the owner-shard partition ("Divide D(i) by N"; AMB-8):
+ *   c = ceil(n/world); len = roundup(c, GDRAA_SHARD_QUANTUM);
+ *   off_r = min(rank*len, n); len_r = min(len, n - off_r).
+ * Pure host function; usable before gdraa_init.  off/len: host pointers (outputs).
+ * Errors: EINVAL (n == 0, world or rank out of range, NULL outputs).
+ */
+int gdraa_shard(int world, int rank, size_t n, size_t *off, size_t *len);
+
+typedef struct {
+    uint64_t calls;            /* collective calls completed on the device (device counter) */
+    uint64_t sync_waits;       /* device barrier completions: 2 per call when world >= 2     */
+    uint64_t rs_bytes_in;      /* algorithmic reduce bytes pulled from peers (Eq. 2)         */
+    uint64_t rs_bytes_out;     /* algorithmic reduce bytes peers pulled from us (Eq. 1)      */
+    uint64_t ag_bytes_out;     /* algorithmic broadcast bytes pushed to peers                */
+    uint64_t ag_bytes_in;      /* algorithmic broadcast bytes peers pushed to us             */
+    uint64_t adds;             /* aggregation adds (Eq. 3, first term)                       */
+    uint64_t divides;          /* aggregation divides (Eq. 3, second term)                   */
+    uint64_t launches;         /* kernels launched by this library                           */
+} gdraa_stats_t;
+
+/*
+ * gdraa_get_stats -- counters of this rank since gdraa_init.  Synchronises the device
+ * to read the device-side counters.  out: host pointer.  Errors: EINVAL, ESTATE, ECUDA.
+ */
+int gdraa_get_stats(gdraa_stats_t *out);
+
+/*
+ * gdraa_finalize -- leave the communicator: synchronises the device, unmaps peer
+ * buffers, frees the signal pads, tells the job server goodbye.  Returns a sticky
+ * error if one is pending (the state is released either way).
+ */
+int gdraa_finalize(void);
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char *gdraa_last_error(void);
+
+/* Library version string (also names the compile target, e.g. "sm_100a"). */
+const char *gdraa_version(void);
+
+/*
+ * Virtual ranks on ONE GPU (test and emulation entry points).  The same device code
+ * as above runs `world` ranks inside ONE cooperative kernel launch: rank r's CTAs use
+ * rank p's buffers through plain device pointers instead of IPC mappings, and the two
+ * synchronisations run through per-rank signal pads in local memory.  This is how
+ * N > 1 is exercised on a single B200 (profiling guide: never run mutually waiting
+ * kernels as separate launches on one GPU).  No gdraa_init is needed.
+ *   world: 1..GDRAA_MAX_WORLD; bufs/w/g/v: HOST arrays of `world` device pointers
+ *   (rank p's buffer at index p), all distinct, 16-byte aligned, n elements.
+ *   Semantics per rank are exactly those of gdraa_allreduce_mean / gdraa_sgd_step.
+ * Errors: EINVAL, ECUDA, ETIMEOUT (returned by a later vr call).
+ */
+int gdraa_vr_allreduce_mean(int world, void *const *bufs, size_t n, int dtype,
+                            gdraa_stream_t s);
+int gdraa_vr_sgd_step(int world, float *const *w, const void *const *g, float *const *v,
+                      size_t n, int dtype, float lr, float mom, gdraa_stream_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GDRAA_H */

@@ -1,0 +1,70 @@
+// gdraa_internal.h -- types shared by the host runtime (gdraa_runtime.cu) and the
+// sm_100a kernels (gdraa_kernels.cu).  Not part of the ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "gdraa.h"
+
+namespace gdraa {
+
+constexpr int kMaxWorld = GDRAA_MAX_WORLD;
+constexpr uint64_t kQuantum = GDRAA_SHARD_QUANTUM;
+
+// Signal pad of one rank (device memory, exported to peers over CUDA IPC).  Peers write
+// only `entry[their rank]` and `exit[their rank]`; everything from `epoch` on is written
+// by the owning rank only.  Each array sits on its own 128-byte line.
+struct alignas(128) Pad {
+    uint64_t entry[kMaxWorld];     // paper "2nd synchronization" (Alg. 1)
+    uint64_t _p0[16 - kMaxWorld];
+    uint64_t exit[kMaxWorld];      // paper "1st synchronization" (Alg. 1)
+    uint64_t _p1[16 - kMaxWorld];
+    uint64_t epoch;                // completed collective calls (device-resident)
+    uint64_t calls;
+    uint64_t sync_waits;
+    uint32_t arrive;               // CTA arrival counter of the running call
+    uint32_t _p2;
+    uint64_t _p3[12];
+};
+static_assert(sizeof(Pad) % 128 == 0, "pad layout");
+
+// Host-mapped failure record (written by the device on a barrier timeout).
+struct ErrBlock {
+    volatile int32_t code;                   // 0 or GDRAA_ETIMEOUT
+    volatile int32_t phase;                  // 1 = entry barrier, 2 = exit barrier
+    volatile uint32_t missing[kMaxWorld];    // missing[p] = 1 if rank p never arrived
+    volatile int32_t vrank;                  // the (virtual) rank that timed out
+};
+
+// Kernel parameters (passed by value).  Row vr describes virtual rank vr: one row in
+// multi-process mode (gridDim.y == 1, rank = rank0), `world` rows in the single-GPU
+// virtual-rank mode (gridDim.y == world, rank = blockIdx.y).
+struct KParams {
+    int world;
+    int rank0;
+    uint64_t n;          // elements
+    uint64_t blk;        // shard length (Q-aligned ceil(n/world))
+    float lr, mom;
+    uint64_t timeout_ns;
+    const void *src[kMaxWorld][kMaxWorld];   // [vr][p]: rank p's g (or buf) seen from vr
+    void *dst[kMaxWorld][kMaxWorld];         // [vr][p]: rank p's w (or buf) seen from vr
+    float *v[kMaxWorld];                     // [vr]: local momentum buffer
+    Pad *pad[kMaxWorld][kMaxWorld];          // [vr][p]: rank p's pad seen from vr
+    ErrBlock *err;                           // host-mapped (device alias)
+    volatile uint64_t *done[kMaxWorld];      // host-mapped done flags (device alias) or null
+};
+
+enum Mode { kMean = 0, kSgd = 1 };
+
+// Launch the fused kernel.  grid_x CTAs per (virtual) rank; vr_rows = gridDim.y.
+// cooperative: use cudaLaunchCooperativeKernel (required when vr_rows > 1).
+cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows,
+                         bool cooperative, cudaStream_t s, int *grid_x_out);
+
+// Max co-resident CTAs of the kernel for (dtype, mode, world) on this device.
+int max_ctas(int dtype, int mode, int world);
+
+}  // namespace gdraa

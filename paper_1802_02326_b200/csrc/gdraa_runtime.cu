@@ -1,0 +1,696 @@
+// gdraa_runtime.cu -- host runtime behind include/gdraa.h.
+//
+// Owns: the job-server connection (control plane), CUDA IPC registration of the
+// caller's buffers (the analogue of P:123's ibv_reg_mr), the signal pads that carry the
+// two synchronisations, the host-mapped go/done and failure pages, sticky errors and
+// counters.  Each collective call validates on the host, then enqueues exactly one
+// kernel (gdraa_kernels.cu) on the caller's stream: no host synchronisation.
+#include <cuda.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <time.h>
+#include <unistd.h>
+
+#include <cerrno>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "gdraa_internal.h"
+#include "jobserver_proto.h"
+
+namespace gdraa {
+namespace {
+
+thread_local std::string t_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            return fail(GDRAA_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));    \
+    } while (0)
+
+uint64_t now_ns() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return static_cast<uint64_t>(ts.tv_sec) * 1000000000ull + ts.tv_nsec;
+}
+
+uint64_t env_u64(const char *name, uint64_t dflt) {
+    const char *v = std::getenv(name);
+    if (v == nullptr || *v == 0) return dflt;
+    return std::strtoull(v, nullptr, 10);
+}
+
+size_t elem_size(int dtype) { return dtype == GDRAA_F32 ? 4 : 2; }
+
+// Q-aligned ceil partition (AMB-8).
+void partition(uint64_t n, int world, int rank, uint64_t *blk, uint64_t *off, uint64_t *len) {
+    const uint64_t c = (n + world - 1) / world;
+    const uint64_t b = (c + kQuantum - 1) / kQuantum * kQuantum;
+    uint64_t o = static_cast<uint64_t>(rank) * b;
+    if (o > n) o = n;
+    *blk = b;
+    *off = o;
+    *len = b < n - o ? b : n - o;
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point (no -lcuda needed).
+using GetRangeFn = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+GetRangeFn get_range_fn() {
+    static GetRangeFn fn = nullptr;
+    if (fn == nullptr) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<GetRangeFn>(p);
+    }
+    return fn;
+}
+
+// ---------------------------------------------------------------------------------
+// Job-server client
+// ---------------------------------------------------------------------------------
+bool io_all(int fd, void *buf, size_t n, bool rd, uint64_t deadline_ns) {
+    char *p = static_cast<char *>(buf);
+    while (n > 0) {
+        if (rd) {
+            timeval tv{};
+            uint64_t left = deadline_ns > now_ns() ? deadline_ns - now_ns() : 0;
+            if (left == 0) return false;
+            tv.tv_sec = left / 1000000000ull;
+            tv.tv_usec = (left % 1000000000ull) / 1000;
+            setsockopt(fd, SOL_SOCKET, SO_RCVTIMEO, &tv, sizeof tv);
+        }
+        ssize_t k = rd ? ::recv(fd, p, n, 0) : ::send(fd, p, n, MSG_NOSIGNAL);
+        if (k == 0) return false;
+        if (k < 0) {
+            if (errno == EINTR) continue;
+            return false;
+        }
+        p += k;
+        n -= static_cast<size_t>(k);
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------------------------
+// State
+// ---------------------------------------------------------------------------------
+struct Registration {
+    void *local = nullptr;
+    size_t n = 0;
+    int dtype = 0;
+    void *peer[kMaxWorld] = {};
+};
+
+struct State {
+    bool inited = false;
+    int world = 0, rank = 0, device = 0;
+    int sock = -1;
+    proto::ShmPage *page = nullptr;     // shared go/done page (host)
+    bool page_registered = false;
+    bool page_owned = false;            // world == 1 without a job server: our own page
+    Pad *pad = nullptr;
+    Pad *peer_pad[kMaxWorld] = {};
+    ErrBlock *err_h = nullptr, *err_d = nullptr;
+    volatile uint64_t *done_d = nullptr;
+    std::vector<Registration> regs;
+    std::map<std::pair<int, std::string>, void *> opened;   // (peer, handle) -> base
+    uint32_t reg_seq = 0;
+    uint64_t timeout_ns = 30000000000ull;
+    bool gated = false;
+    uint64_t issued = 0;
+    bool fatal = false;
+    int fatal_code = 0;
+    std::string fatal_msg;
+    gdraa_stats_t host{};
+};
+
+State g;
+std::mutex g_mu;
+
+int send_msg(uint16_t kind, uint32_t seq, const void *payload, uint32_t len) {
+    proto::Hdr h{proto::kMagic, kind, static_cast<uint16_t>(g.rank), len, seq};
+    const uint64_t dl = now_ns() + 10000000000ull;
+    if (!io_all(g.sock, &h, sizeof h, false, dl) ||
+        (len && !io_all(g.sock, const_cast<void *>(payload), len, false, dl)))
+        return fail(GDRAA_EJOBSERVER, "job server: send failed: %s", std::strerror(errno));
+    return GDRAA_OK;
+}
+
+// Receive one message; FAIL from the server becomes an error with its message.
+int recv_msg(uint16_t want, uint32_t seq, void *payload, uint32_t len, uint64_t timeout_ns,
+             uint16_t *got_kind = nullptr) {
+    proto::Hdr h;
+    const uint64_t dl = now_ns() + timeout_ns;
+    if (!io_all(g.sock, &h, sizeof h, true, dl))
+        return fail(GDRAA_EJOBSERVER, "job server: no reply (waiting for kind %u): %s", want,
+                    errno ? std::strerror(errno) : "closed");
+    std::vector<char> body(h.len);
+    if (h.len && !io_all(g.sock, body.data(), h.len, true, dl))
+        return fail(GDRAA_EJOBSERVER, "job server: truncated reply");
+    if (got_kind) *got_kind = h.kind;
+    if (h.magic != proto::kMagic) return fail(GDRAA_EJOBSERVER, "job server: bad magic");
+    if (h.kind == proto::FAIL || h.kind == proto::REG_ERR) {
+        proto::Fail f{};
+        std::memcpy(&f, body.data(), std::min(sizeof f, body.size()));
+        f.msg[sizeof f.msg - 1] = 0;
+        return fail(f.code ? f.code : GDRAA_EJOBSERVER, "job server: %s", f.msg);
+    }
+    if (h.kind != want || h.seq != seq || h.len != len)
+        return fail(GDRAA_EJOBSERVER, "job server: unexpected reply kind %u seq %u len %u",
+                    h.kind, h.seq, h.len);
+    if (len) std::memcpy(payload, body.data(), len);
+    return GDRAA_OK;
+}
+
+int connect_jobserver(const char *path, uint64_t timeout_ns) {
+    const uint64_t dl = now_ns() + timeout_ns;
+    sockaddr_un addr{};
+    addr.sun_family = AF_UNIX;
+    if (std::strlen(path) >= sizeof addr.sun_path)
+        return fail(GDRAA_EINVAL, "GDRAA_JOBSERVER path too long");
+    std::snprintf(addr.sun_path, sizeof addr.sun_path, "%s", path);
+    while (true) {
+        int fd = ::socket(AF_UNIX, SOCK_STREAM, 0);
+        if (fd < 0) return fail(GDRAA_EJOBSERVER, "socket: %s", std::strerror(errno));
+        if (::connect(fd, reinterpret_cast<sockaddr *>(&addr), sizeof addr) == 0) {
+            g.sock = fd;
+            return GDRAA_OK;
+        }
+        ::close(fd);
+        if (now_ns() > dl)
+            return fail(GDRAA_EJOBSERVER, "cannot connect to job server at %s: %s", path,
+                        std::strerror(errno));
+        usleep(20000);
+    }
+}
+
+// Exchange one registration record with every rank through the job server.
+int exchange(const proto::Reg &mine, proto::RegOk *all) {
+    const uint32_t seq = ++g.reg_seq;
+    int rc = send_msg(proto::REG, seq, &mine, sizeof mine);
+    if (rc) return rc;
+    return recv_msg(proto::REG_OK, seq, all, sizeof *all,
+                    env_u64("GDRAA_CONNECT_TIMEOUT_MS", 120000) * 1000000ull);
+}
+
+// Export the allocation holding [ptr, ptr+bytes) and map every peer's counterpart.
+int ipc_exchange(void *ptr, size_t bytes, uint64_t n, int dtype, int what,
+                 void *out_peer[kMaxWorld]) {
+    GetRangeFn range = get_range_fn();
+    if (range == nullptr) return fail(GDRAA_ECUDA, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+        return fail(GDRAA_EINVAL, "pointer %p is not device memory of this context", ptr);
+    const uint64_t offset = reinterpret_cast<uint64_t>(ptr) - base;
+    if (offset + bytes > size)
+        return fail(GDRAA_EINVAL, "buffer [%p, +%zu) exceeds its allocation (%zu bytes)", ptr,
+                    bytes, size);
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base));
+    if (e != cudaSuccess)
+        return fail(GDRAA_ECUDA,
+                    "cudaIpcGetMemHandle: %s (buffers must come from cudaMalloc; with PyTorch "
+                    "keep PYTORCH_CUDA_ALLOC_CONF expandable_segments off)",
+                    cudaGetErrorString(e));
+    proto::Reg mine{};
+    mine.n = n;
+    mine.dtype = dtype;
+    mine.what = what;
+    mine.offset = offset;
+    static_assert(sizeof(h) == sizeof(mine.handle), "IPC handle size");
+    std::memcpy(mine.handle, &h, sizeof h);
+    proto::RegOk all{};
+    int rc = exchange(mine, &all);
+    if (rc) return rc;
+    for (int p = 0; p < g.world; ++p) {
+        if (p == g.rank) {
+            out_peer[p] = ptr;
+            continue;
+        }
+        std::string key(reinterpret_cast<const char *>(all.regs[p].handle), 64);
+        auto it = g.opened.find({p, key});
+        void *pbase = nullptr;
+        if (it != g.opened.end()) {
+            pbase = it->second;
+        } else {
+            cudaIpcMemHandle_t ph;
+            std::memcpy(&ph, all.regs[p].handle, sizeof ph);
+            e = cudaIpcOpenMemHandle(&pbase, ph, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess)
+                return fail(GDRAA_ECUDA, "cudaIpcOpenMemHandle(rank %d): %s", p,
+                            cudaGetErrorString(e));
+            g.opened[{p, key}] = pbase;
+        }
+        out_peer[p] = static_cast<char *>(pbase) + all.regs[p].offset;
+    }
+    return GDRAA_OK;
+}
+
+int check_sticky() {
+    if (!g.inited) return fail(GDRAA_ESTATE, "gdraa_init has not been called");
+    if (g.fatal) return fail(g.fatal_code, "%s", g.fatal_msg.c_str());
+    if (g.err_h != nullptr && g.err_h->code != 0) {
+        std::string miss;
+        for (int p = 0; p < kMaxWorld; ++p)
+            if (g.err_h->missing[p]) miss += (miss.empty() ? "" : ",") + std::to_string(p);
+        char buf[256];
+        std::snprintf(buf, sizeof buf,
+                      "peer timeout in the %s synchronisation after %llu ms: missing rank(s) %s",
+                      g.err_h->phase == 1 ? "entry (paper 2nd)" : "exit (paper 1st)",
+                      (unsigned long long)(g.timeout_ns / 1000000ull), miss.c_str());
+        g.fatal = true;
+        g.fatal_code = GDRAA_ETIMEOUT;
+        g.fatal_msg = buf;
+        return fail(GDRAA_ETIMEOUT, "%s", buf);
+    }
+    if (g.page != nullptr && !g.page_owned && g.page->abort) {
+        g.fatal = true;
+        g.fatal_code = GDRAA_EJOBSERVER;
+        g.fatal_msg = "job server reports rank " + std::to_string(g.page->dead_rank) + " died";
+        return fail(GDRAA_EJOBSERVER, "%s", g.fatal_msg.c_str());
+    }
+    return GDRAA_OK;
+}
+
+const Registration *find_reg(const void *ptr) {
+    for (const auto &r : g.regs)
+        if (r.local == ptr) return &r;
+    return nullptr;
+}
+
+int wait_go() {
+    if (!g.gated || g.page == nullptr) return GDRAA_OK;
+    const uint64_t want = g.issued + 1;
+    const uint64_t dl = now_ns() + g.timeout_ns;
+    while (g.page->go[g.rank] < want) {
+        if (g.page->abort) return check_sticky();
+        if (now_ns() > dl) return fail(GDRAA_ETIMEOUT, "gated: no go(%llu) from job server",
+                                       (unsigned long long)want);
+        usleep(5);
+    }
+    return GDRAA_OK;
+}
+
+void fill_common(KParams &p, uint64_t n) {
+    std::memset(&p, 0, sizeof p);
+    p.world = g.world;
+    p.rank0 = g.rank;
+    p.n = n;
+    uint64_t off, len;
+    partition(n, g.world, g.rank, &p.blk, &off, &len);
+    p.timeout_ns = g.timeout_ns;
+    for (int q = 0; q < g.world; ++q) p.pad[0][q] = g.peer_pad[q];
+    p.err = g.err_d;
+    p.done[0] = g.done_d;
+}
+
+void account(uint64_t n, int dtype_g, bool sgd) {
+    uint64_t blk, off, len;
+    partition(n, g.world, g.rank, &blk, &off, &len);
+    const uint64_t sg = elem_size(dtype_g), sw = sgd ? 4 : sg, n1 = g.world - 1;
+    g.host.rs_bytes_in += sg * n1 * len;
+    g.host.rs_bytes_out += sg * (n - len);
+    g.host.ag_bytes_out += sw * n1 * len;
+    g.host.ag_bytes_in += sw * (n - len);
+    g.host.adds += n1 * len;
+    g.host.divides += len;
+    g.host.launches += 1;
+}
+
+int launch(const KParams &p, int dtype, int mode, cudaStream_t s) {
+    int gx = 0;
+    cudaError_t e = launch_gdraa(p, dtype, mode, 1, false, s, &gx);
+    if (e != cudaSuccess) return fail(GDRAA_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
+    g.issued += 1;
+    return GDRAA_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// Virtual ranks on one GPU: pads per (device, world), one failure page per device.
+// ---------------------------------------------------------------------------------
+struct VrDevice {
+    Pad *pads[kMaxWorld + 1] = {};      // pads[world] -> `world` consecutive Pads
+    ErrBlock *err_h = nullptr, *err_d = nullptr;
+};
+std::map<int, VrDevice> g_vr;
+
+int vr_prepare(int world, VrDevice **out) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    VrDevice &d = g_vr[dev];
+    if (d.err_h == nullptr) {
+        void *h = nullptr;
+        CUDA_TRY(cudaHostAlloc(&h, sizeof(ErrBlock), cudaHostAllocMapped | cudaHostAllocPortable));
+        std::memset(h, 0, sizeof(ErrBlock));
+        d.err_h = static_cast<ErrBlock *>(h);
+        void *dp = nullptr;
+        CUDA_TRY(cudaHostGetDevicePointer(&dp, h, 0));
+        d.err_d = static_cast<ErrBlock *>(dp);
+    }
+    if (d.err_h->code != 0) {
+        std::string miss;
+        for (int p = 0; p < kMaxWorld; ++p)
+            if (d.err_h->missing[p]) miss += (miss.empty() ? "" : ",") + std::to_string(p);
+        return fail(GDRAA_ETIMEOUT, "virtual-rank peer timeout (phase %d, vrank %d): missing %s",
+                    d.err_h->phase, d.err_h->vrank, miss.c_str());
+    }
+    if (d.pads[world] == nullptr) {
+        void *pp = nullptr;
+        CUDA_TRY(cudaMalloc(&pp, sizeof(Pad) * world));
+        CUDA_TRY(cudaMemset(pp, 0, sizeof(Pad) * world));
+        d.pads[world] = static_cast<Pad *>(pp);
+    }
+    *out = &d;
+    return GDRAA_OK;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int vr_run(int world, const void *const *src, void *const *dst, float *const *v, size_t n,
+           int dtype, float lr, float mom, int mode, cudaStream_t s) {
+    if (world < 1 || world > kMaxWorld) return fail(GDRAA_EINVAL, "world %d out of [1,%d]", world, kMaxWorld);
+    if (n == 0) return fail(GDRAA_EINVAL, "n must be >= 1");
+    if (dtype != GDRAA_F32 && dtype != GDRAA_BF16) return fail(GDRAA_EINVAL, "bad dtype %d", dtype);
+    if (src == nullptr || dst == nullptr || (mode == kSgd && v == nullptr))
+        return fail(GDRAA_EINVAL, "null pointer array");
+    if (mode == kSgd && !(std::isfinite(lr) && std::isfinite(mom)))
+        return fail(GDRAA_EINVAL, "lr and mom must be finite");
+    for (int q = 0; q < world; ++q) {
+        if (src[q] == nullptr || dst[q] == nullptr || !aligned16(src[q]) || !aligned16(dst[q]) ||
+            (mode == kSgd && (v[q] == nullptr || !aligned16(v[q]))))
+            return fail(GDRAA_EINVAL, "rank %d: null or non-16-byte-aligned buffer", q);
+    }
+    VrDevice *d = nullptr;
+    int rc = vr_prepare(world, &d);
+    if (rc) return rc;
+    KParams p;
+    std::memset(&p, 0, sizeof p);
+    p.world = world;
+    p.rank0 = 0;
+    p.n = n;
+    uint64_t off, len;
+    partition(n, world, 0, &p.blk, &off, &len);
+    p.lr = lr;
+    p.mom = mom;
+    p.timeout_ns = env_u64("GDRAA_TIMEOUT_MS", 30000) * 1000000ull;
+    for (int r = 0; r < world; ++r) {
+        for (int q = 0; q < world; ++q) {
+            p.src[r][q] = src[q];
+            p.dst[r][q] = dst[q];
+            p.pad[r][q] = d->pads[world] + q;
+        }
+        p.v[r] = mode == kSgd ? v[r] : nullptr;
+    }
+    p.err = d->err_d;
+    int gx = 0;
+    cudaError_t e = launch_gdraa(p, dtype, mode, world, true, s, &gx);
+    if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr kernel launch: %s", cudaGetErrorString(e));
+    return GDRAA_OK;
+}
+
+}  // namespace
+}  // namespace gdraa
+
+using namespace gdraa;
+
+extern "C" {
+
+const char *gdraa_last_error(void) { return t_err.c_str(); }
+
+const char *gdraa_version(void) { return "gdraa 0.1.0 (sm_100a)"; }
+
+int gdraa_shard(int world, int rank, size_t n, size_t *off, size_t *len) {
+    if (off == nullptr || len == nullptr) return fail(GDRAA_EINVAL, "null output pointer");
+    if (n == 0) return fail(GDRAA_EINVAL, "n must be >= 1");
+    if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
+        return fail(GDRAA_EINVAL, "world %d / rank %d out of range", world, rank);
+    uint64_t b, o, l;
+    partition(n, world, rank, &b, &o, &l);
+    *off = o;
+    *len = l;
+    return GDRAA_OK;
+}
+
+int gdraa_init(int world, int rank) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g.inited) return fail(GDRAA_ESTATE, "already initialised (world %d, rank %d)", g.world, g.rank);
+    if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
+        return fail(GDRAA_EINVAL, "world %d / rank %d out of range [1,%d]", world, rank, kMaxWorld);
+    State s;
+    g = s;
+    g.world = world;
+    g.rank = rank;
+    g.timeout_ns = env_u64("GDRAA_TIMEOUT_MS", 30000) * 1000000ull;
+    CUDA_TRY(cudaGetDevice(&g.device));
+    int cc_major = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, g.device));
+    if (cc_major != 10) return fail(GDRAA_ECUDA, "device %d is not sm_100 (compute %d.x)", g.device, cc_major);
+
+    auto cleanup_fail = [&](int rc) {
+        if (g.sock >= 0) ::close(g.sock);
+        g.sock = -1;
+        return rc;
+    };
+
+    // Signal pad and failure page.
+    void *pp = nullptr;
+    CUDA_TRY(cudaMalloc(&pp, sizeof(Pad)));
+    CUDA_TRY(cudaMemset(pp, 0, sizeof(Pad)));
+    CUDA_TRY(cudaDeviceSynchronize());
+    g.pad = static_cast<Pad *>(pp);
+    void *eh = nullptr;
+    CUDA_TRY(cudaHostAlloc(&eh, sizeof(ErrBlock), cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(eh, 0, sizeof(ErrBlock));
+    g.err_h = static_cast<ErrBlock *>(eh);
+    void *ed = nullptr;
+    CUDA_TRY(cudaHostGetDevicePointer(&ed, eh, 0));
+    g.err_d = static_cast<ErrBlock *>(ed);
+
+    const char *js = std::getenv("GDRAA_JOBSERVER");
+    if (world > 1 && (js == nullptr || *js == 0))
+        return fail(GDRAA_EJOBSERVER, "world > 1 needs GDRAA_JOBSERVER=<socket path> "
+                                      "(start paper_1802_02326_b200.jobserver)");
+    if (js != nullptr && *js != 0) {
+        int rc = connect_jobserver(js, env_u64("GDRAA_CONNECT_TIMEOUT_MS", 120000) * 1000000ull);
+        if (rc) return rc;
+        proto::Hello hello{};
+        hello.world = world;
+        hello.pid = static_cast<int32_t>(getpid());
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, g.device) == cudaSuccess)
+            std::memcpy(hello.uuid, &prop.uuid, sizeof hello.uuid);
+        rc = send_msg(proto::HELLO, 0, &hello, sizeof hello);
+        if (rc) return cleanup_fail(rc);
+        proto::HelloOk ok{};
+        rc = recv_msg(proto::HELLO_OK, 0, &ok, sizeof ok,
+                      env_u64("GDRAA_CONNECT_TIMEOUT_MS", 120000) * 1000000ull);
+        if (rc) return cleanup_fail(rc);
+        g.gated = ok.gated != 0;
+        int fd = shm_open(ok.shm_name, O_RDWR, 0);
+        if (fd < 0) return cleanup_fail(fail(GDRAA_EJOBSERVER, "shm_open(%s): %s", ok.shm_name, std::strerror(errno)));
+        void *mem = mmap(nullptr, 4096, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        ::close(fd);
+        if (mem == MAP_FAILED) return cleanup_fail(fail(GDRAA_EJOBSERVER, "mmap shm: %s", std::strerror(errno)));
+        g.page = static_cast<proto::ShmPage *>(mem);
+    } else {
+        void *mem = mmap(nullptr, 4096, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_ANONYMOUS, -1, 0);
+        if (mem == MAP_FAILED) return fail(GDRAA_ECUDA, "mmap: %s", std::strerror(errno));
+        std::memset(mem, 0, 4096);
+        g.page = static_cast<proto::ShmPage *>(mem);
+        g.page_owned = true;
+    }
+    // Kernels write done[rank] ("IterDone") straight into the shared page.
+    cudaError_t e = cudaHostRegister(g.page, 4096, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) return cleanup_fail(fail(GDRAA_ECUDA, "cudaHostRegister(go/done page): %s", cudaGetErrorString(e)));
+    g.page_registered = true;
+    void *pd = nullptr;
+    CUDA_TRY(cudaHostGetDevicePointer(&pd, g.page, 0));
+    g.done_d = &static_cast<proto::ShmPage *>(pd)->done[rank];
+
+    // Exchange signal pads (registration sequence 1).
+    void *peers[kMaxWorld] = {};
+    if (world > 1) {
+        int rc = ipc_exchange(g.pad, sizeof(Pad), sizeof(Pad), -1, 0, peers);
+        if (rc) return cleanup_fail(rc);
+    } else {
+        peers[0] = g.pad;
+    }
+    for (int p = 0; p < world; ++p) g.peer_pad[p] = static_cast<Pad *>(peers[p]);
+    g.inited = true;
+    return GDRAA_OK;
+}
+
+int gdraa_register(void *buf, size_t n, int dtype) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int rc = check_sticky();
+    if (rc) return rc;
+    if (buf == nullptr || n == 0) return fail(GDRAA_EINVAL, "null buffer or n == 0");
+    if (dtype != GDRAA_F32 && dtype != GDRAA_BF16) return fail(GDRAA_EINVAL, "bad dtype %d", dtype);
+    if (!aligned16(buf)) return fail(GDRAA_EINVAL, "buffer %p is not 16-byte aligned", buf);
+    if (find_reg(buf) != nullptr) return fail(GDRAA_EINVAL, "buffer %p already registered", buf);
+    Registration r;
+    r.local = buf;
+    r.n = n;
+    r.dtype = dtype;
+    if (g.world > 1) {
+        rc = ipc_exchange(buf, n * elem_size(dtype), n, dtype, 1, r.peer);
+        if (rc) return rc;
+    } else {
+        cudaPointerAttributes a;
+        CUDA_TRY(cudaPointerGetAttributes(&a, buf));
+        if (a.type != cudaMemoryTypeDevice) return fail(GDRAA_EINVAL, "buffer %p is not device memory", buf);
+        r.peer[0] = buf;
+    }
+    g.regs.push_back(r);
+    return GDRAA_OK;
+}
+
+int gdraa_deregister(void *buf) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.inited) return fail(GDRAA_ESTATE, "gdraa_init has not been called");
+    for (auto it = g.regs.begin(); it != g.regs.end(); ++it) {
+        if (it->local == buf) {
+            g.regs.erase(it);
+            return GDRAA_OK;
+        }
+    }
+    return fail(GDRAA_ENOTREG, "buffer %p is not registered", buf);
+}
+
+int gdraa_allreduce_mean(void *buf, gdraa_stream_t s) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int rc = check_sticky();
+    if (rc) return rc;
+    const Registration *r = find_reg(buf);
+    if (r == nullptr) return fail(GDRAA_ENOTREG, "buffer %p is not registered", buf);
+    rc = wait_go();
+    if (rc) return rc;
+    KParams p;
+    fill_common(p, r->n);
+    for (int q = 0; q < g.world; ++q) {
+        p.src[0][q] = r->peer[q];
+        p.dst[0][q] = r->peer[q];
+    }
+    rc = launch(p, r->dtype, kMean, reinterpret_cast<cudaStream_t>(s));
+    if (rc) return rc;
+    account(r->n, r->dtype, false);
+    return GDRAA_OK;
+}
+
+int gdraa_sgd_step(float *w, const void *gr, float *v, float lr, float mom, gdraa_stream_t s) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int rc = check_sticky();
+    if (rc) return rc;
+    if (!(std::isfinite(lr) && std::isfinite(mom))) return fail(GDRAA_EINVAL, "lr and mom must be finite");
+    const Registration *rw = find_reg(w);
+    const Registration *rg = find_reg(gr);
+    if (rw == nullptr) return fail(GDRAA_ENOTREG, "w %p is not registered", static_cast<void *>(w));
+    if (rg == nullptr) return fail(GDRAA_ENOTREG, "g %p is not registered", gr);
+    if (rw->dtype != GDRAA_F32) return fail(GDRAA_EINVAL, "w must be registered as GDRAA_F32");
+    if (rw->n != rg->n) return fail(GDRAA_EINVAL, "w (n=%zu) and g (n=%zu) differ in length", rw->n, rg->n);
+    if (rw == rg) return fail(GDRAA_EINVAL, "w and g must be distinct buffers");
+    if (v == nullptr || !aligned16(v)) return fail(GDRAA_EINVAL, "v is null or not 16-byte aligned");
+    rc = wait_go();
+    if (rc) return rc;
+    KParams p;
+    fill_common(p, rw->n);
+    p.lr = lr;
+    p.mom = mom;
+    for (int q = 0; q < g.world; ++q) {
+        p.src[0][q] = rg->peer[q];
+        p.dst[0][q] = rw->peer[q];
+    }
+    p.v[0] = v;
+    rc = launch(p, rg->dtype, kSgd, reinterpret_cast<cudaStream_t>(s));
+    if (rc) return rc;
+    account(rw->n, rg->dtype, true);
+    return GDRAA_OK;
+}
+
+int gdraa_get_stats(gdraa_stats_t *out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (out == nullptr) return fail(GDRAA_EINVAL, "null output");
+    if (!g.inited) return fail(GDRAA_ESTATE, "gdraa_init has not been called");
+    CUDA_TRY(cudaDeviceSynchronize());
+    Pad host;
+    CUDA_TRY(cudaMemcpy(&host, g.pad, sizeof host, cudaMemcpyDeviceToHost));
+    *out = g.host;
+    out->calls = host.calls;
+    out->sync_waits = host.sync_waits;
+    return GDRAA_OK;
+}
+
+int gdraa_finalize(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.inited) return fail(GDRAA_ESTATE, "gdraa_init has not been called");
+    int rc = GDRAA_OK;
+    cudaError_t se = cudaDeviceSynchronize();
+    {
+        int st = check_sticky();
+        if (st) rc = st;
+    }
+    if (se != cudaSuccess && rc == GDRAA_OK) rc = fail(GDRAA_ECUDA, "cudaDeviceSynchronize: %s", cudaGetErrorString(se));
+    std::string keep = t_err;
+    if (g.sock >= 0) {
+        if (send_msg(proto::BYE, 0, nullptr, 0) == GDRAA_OK && !g.fatal) {
+            int brc = recv_msg(proto::BYE_OK, 0, nullptr, 0, 60000000000ull);
+            if (brc && rc == GDRAA_OK) {
+                rc = brc;
+                keep = t_err;
+            }
+        }
+        ::close(g.sock);
+        g.sock = -1;
+    }
+    for (auto &kv : g.opened) cudaIpcCloseMemHandle(kv.second);
+    g.opened.clear();
+    if (g.pad) cudaFree(g.pad);
+    if (g.page_registered) cudaHostUnregister(g.page);
+    if (g.page) munmap(g.page, 4096);
+    if (g.err_h) cudaFreeHost(g.err_h);
+    State s;
+    g = s;
+    t_err = keep;
+    return rc;
+}
+
+int gdraa_vr_allreduce_mean(int world, void *const *bufs, size_t n, int dtype, gdraa_stream_t s) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return vr_run(world, reinterpret_cast<const void *const *>(bufs), bufs, nullptr, n, dtype, 0.f,
+                  0.f, kMean, reinterpret_cast<cudaStream_t>(s));
+}
+
+int gdraa_vr_sgd_step(int world, float *const *w, const void *const *g_, float *const *v, size_t n,
+                      int dtype, float lr, float mom, gdraa_stream_t s) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return vr_run(world, g_, reinterpret_cast<void *const *>(w), v, n, dtype, lr, mom, kSgd,
+                  reinterpret_cast<cudaStream_t>(s));
+}
+
+}  // extern "C"

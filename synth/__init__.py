@@ -96,9 +96,35 @@ def neg_zero_segment(seed, n):
     return int(u64(seed, 0, S_SEG, 1)[0] % np.uint64(nseg))
 
 
+_CHUNK = 1 << 20
+
+
+def _chunked(fn, n, start, dtype):
+    """Evaluate fn(count, start) over [start, start+n) in 1M-element chunks on a thread
+    pool (numpy releases the GIL).  Values are counter-based, so chunking is invisible."""
+    if n <= _CHUNK:
+        return fn(n, start)
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+    out = np.empty(n, dtype=dtype)
+    spans = [(a, min(_CHUNK, n - a)) for a in range(0, n, _CHUNK)]
+
+    def run(span):
+        a, c = span
+        out[a:a + c] = fn(c, start + a)
+
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
+        list(ex.map(run, spans))
+    return out
+
+
 def grad_like(seed, rank, n, start=0):
     """Gradient-like float32 for indices [start, start+n): N(0,1) x 10^U(-6,-1) per
     4096-element segment (per-layer scales), 1% exact +0.0 and 0.1% -0.0."""
+    return _chunked(lambda c, s: _grad_like(seed, rank, c, s), n, start, np.float32)
+
+
+def _grad_like(seed, rank, n, start):
     seg = np.arange(start, start + n, dtype=np.uint64) // np.uint64(SEGMENT)
     with np.errstate(over="ignore"):
         e = _splitmix64(_key(seed, rank, S_SCALE) + seg * np.uint64(0xD1B54A32D192ED03))
@@ -121,7 +147,8 @@ def grad_like_full(seed, rank, n):
 
 def w_like(seed, n):
     """Weights ~ N(0, 0.05^2), identical on every rank."""
-    return (normal(seed, 0, S_W, n) * 0.05).astype(np.float32)
+    return _chunked(lambda c, s: (normal(seed, 0, S_W, c, s) * 0.05).astype(np.float32),
+                    n, 0, np.float32)
 
 
 def to_bf16_bits_trunc(x: np.ndarray) -> np.ndarray:

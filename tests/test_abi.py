@@ -1,0 +1,87 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every symbol
+include/gdraa.h declares, carries sm_100a SASS, and its host logic (the partition, the
+argument checks that precede any CUDA call) behaves as documented."""
+import os
+import re
+import subprocess
+
+import pytest
+
+import oracle
+import synth
+from paper_1802_02326_b200 import gdraa
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "gdraa.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gdraa_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert "gdraa_sgd_step" in syms and "gdraa_allreduce_mean" in syms
+    out = subprocess.run(["nm", "-D", "--defined-only", gdraa.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (gdraa_\w+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    assert sorted(gdraa.EXPORTED) == syms
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", gdraa.LIB_PATH],
+                         capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in out, out
+    assert "sm_100a" in gdraa.gdraa_version()
+
+
+def test_no_oracle_in_product():
+    """The product never links or imports the oracle (and vice versa)."""
+    out = subprocess.run(["nm", "-D", gdraa.LIB_PATH], capture_output=True, text=True).stdout
+    assert "oracle_" not in out
+    pkg = os.path.join(ROOT, "paper_1802_02326_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "gdraa_oracle" not in txt, f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".py", ".c", ".h")):
+            txt = open(os.path.join(ROOT, "oracle", f)).read()
+            assert not re.search(r"^\s*(import|from)\s+paper_1802_02326_b200", txt, re.M), f
+            assert not re.search(r'#include\s+"gdraa(_internal)?\.h"', txt), f
+
+
+@pytest.mark.parametrize("N", range(1, 9))
+def test_shard_matches_oracle_partition(N):
+    for L in (1, 2, 63, 64, 65, 1000, 4096 * N + 7, 1 << 20, synth.L_R50, synth.L_R101):
+        for r in range(N):
+            assert gdraa.gdraa_shard(N, r, L) == oracle.partition(L, N, r, Q=64)
+
+
+def test_shard_alignment():
+    for N in range(1, 9):
+        for r in range(N):
+            off, ln = gdraa.gdraa_shard(N, r, synth.L_R50)
+            assert off % gdraa.GDRAA_SHARD_QUANTUM == 0
+
+
+@pytest.mark.parametrize("args", [(0, 0, 10), (9, 0, 10), (2, 2, 10), (2, -1, 10), (2, 0, 0)])
+def test_shard_rejects(args):
+    with pytest.raises(gdraa.GdraaError) as e:
+        gdraa.gdraa_shard(*args)
+    assert e.value.name == "GDRAA_EINVAL"
+
+
+def test_calls_before_init_fail_cleanly():
+    for fn, args in [(gdraa.gdraa_register, (1 << 20, 10, 0)), (gdraa.gdraa_get_stats, ()),
+                     (gdraa.gdraa_finalize, ()), (gdraa.gdraa_deregister, (1 << 20,))]:
+        with pytest.raises(gdraa.GdraaError) as e:
+            fn(*args)
+        assert e.value.name == "GDRAA_ESTATE", fn
+    assert "gdraa_init" in gdraa.gdraa_last_error()

@@ -1,0 +1,259 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Single-GPU coverage of every world size uses the virtual-rank entry points
+(gdraa_vr_*): the same kernel runs N ranks in one cooperative launch on one B200, with
+rank r's CTAs reading and writing rank p's buffers and the two synchronisations going
+through per-rank signal pads.  The multi-process NVLink path is in test_multigpu.py.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests._parity import compare
+from tests.conftest import has_cuda
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_cuda(), reason="needs a CUDA GPU")]
+
+if has_cuda():
+    from paper_1802_02326_b200 import gdraa
+
+DEV = "cuda:0"
+
+
+def to_dev(x, bf16=False, dev=DEV):
+    if bf16:
+        return torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).to(dev).view(torch.bfloat16)
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+
+def from_dev(t):
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def make_grads(family, seed, N, L, bf16):
+    if family == "int":
+        gs = [synth.grad_integer(seed, p, L, bf16=bf16) for p in range(N)]
+    else:
+        gs = [synth.grad_like(seed, p, L) for p in range(N)]
+        k = synth.neg_zero_segment(seed, L)
+        for g in gs:
+            g[k * synth.SEGMENT:(k + 1) * synth.SEGMENT] = np.float32(-0.0)
+    if bf16:
+        gs = [synth.to_bf16_bits_trunc(g) for g in gs]
+    return gs
+
+
+def make_wv(family, seed, L):
+    if family == "int":
+        return synth.w_integer(seed, L), synth.v_integer(seed, L), synth.INT_LR, synth.INT_MOM
+    return synth.w_like(seed, L), np.zeros(L, np.float32), synth.PAPER_LR, synth.PAPER_MOM
+
+
+SIZES = [1, 5, 64, 257, 1000, 70_001, 1 << 20]
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("family", ["int", "like"])
+def test_vr_allreduce_mean(N, dt, family):
+    bf16 = dt == "bf16"
+    for L in SIZES:
+        gs = make_grads(family, 100 + N, N, L, bf16)
+        exp = oracle.allreduce_mean(gs)
+        bufs = [to_dev(g, bf16) for g in gs]
+        gdraa.gdraa_vr_allreduce_mean(bufs)
+        torch.cuda.synchronize()
+        for r in range(N):
+            compare(from_dev(bufs[r]), exp, dt, what=f"mean N={N} L={L} rank {r}")
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 6, 7, 8])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("family", ["int", "like"])
+def test_vr_sgd_step(N, dt, family):
+    bf16 = dt == "bf16"
+    for L in SIZES:
+        gs = make_grads(family, 200 + N, N, L, bf16)
+        w0, v0, lr, mom = make_wv(family, 200 + N, L)
+        if family == "like":
+            v0 = synth.w_like(300 + N, L)          # non-zero momentum state
+        w_exp, v_exp = oracle.sgd_step(gs, w0, v0, lr, mom)
+        g_d = [to_dev(g, bf16) for g in gs]
+        w_d = [to_dev(w0) for _ in range(N)]
+        v_d = [to_dev(v0) for _ in range(N)]
+        gdraa.gdraa_vr_sgd_step(w_d, g_d, v_d, lr, mom)
+        torch.cuda.synchronize()
+        for r in range(N):
+            compare(from_dev(w_d[r]), w_exp, "f32", what=f"w N={N} L={L} rank {r}")
+            off, ln = gdraa.gdraa_shard(N, r, L)
+            vr = from_dev(v_d[r])
+            compare(vr[off:off + ln], v_exp[off:off + ln], "f32", what=f"v N={N} L={L} r{r}")
+            # AMB-19: non-owned momentum entries are untouched
+            keep = np.ones(L, bool)
+            keep[off:off + ln] = False
+            assert np.array_equal(vr[keep].view(np.uint32), v0[keep].view(np.uint32))
+            # AMB-18: g is read only
+            assert np.array_equal(from_dev(g_d[r]), gs[r])
+
+
+@pytest.mark.parametrize("N,dt", [(2, "f32"), (4, "f32"), (8, "bf16")])
+def test_vr_chained_iterations(N, dt):
+    """10 chained steps with fresh gradients each iteration (random family, P:246
+    hyper-parameters), compared after every iteration."""
+    bf16 = dt == "bf16"
+    L = 300_007
+    w, v = synth.w_like(9, L), np.zeros(L, np.float32)
+    w_d = [to_dev(w) for _ in range(N)]
+    v_full = [to_dev(v) for _ in range(N)]
+    for it in range(10):
+        gs = make_grads("like", 1000 + it, N, L, bf16)
+        g_d = [to_dev(g, bf16) for g in gs]
+        w, v = oracle.sgd_step(gs, w, v, synth.PAPER_LR, synth.PAPER_MOM)
+        gdraa.gdraa_vr_sgd_step(w_d, g_d, v_full, synth.PAPER_LR, synth.PAPER_MOM)
+        torch.cuda.synchronize()
+        for r in range(N):
+            compare(from_dev(w_d[r]), w, "f32", what=f"it {it} w rank {r}")
+            off, ln = gdraa.gdraa_shard(N, r, L)
+            compare(from_dev(v_full[r])[off:off + ln], v[off:off + ln], "f32",
+                    what=f"it {it} v rank {r}")
+
+
+def test_vr_determinism_and_partition_independence():
+    """bitwise identical across runs; w' and the mean do not depend on N's
+    partition (same inputs averaged by 4 ranks in two different launches)."""
+    L, N = 1 << 20, 4
+    gs = make_grads("like", 77, N, L, False)
+    outs = []
+    for _ in range(3):
+        bufs = [to_dev(g) for g in gs]
+        gdraa.gdraa_vr_allreduce_mean(bufs)
+        torch.cuda.synchronize()
+        outs.append([from_dev(b) for b in bufs])
+    for run in outs[1:]:
+        for a, b in zip(run, outs[0]):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_vr_full_size_resnet50_bf16_n8():
+    """Config 4 at its stated N=8: ResNet-50 gradients in bf16, fp32 accumulation, fp32
+    master w/v -- full size, every element, both iteration 1 and a chained iteration 2."""
+    N, L = 8, synth.L_R50
+    gs = make_grads("like", 4, N, L, True)
+    w0, v0 = synth.w_like(4, L), np.zeros(L, np.float32)
+    w1, v1 = oracle.sgd_step(gs, w0, v0, synth.PAPER_LR, synth.PAPER_MOM)
+    g_d = [to_dev(g, True) for g in gs]
+    w_d = [to_dev(w0) for _ in range(N)]
+    v_d = [to_dev(v0) for _ in range(N)]
+    gdraa.gdraa_vr_sgd_step(w_d, g_d, v_d, synth.PAPER_LR, synth.PAPER_MOM)
+    torch.cuda.synchronize()
+    for r in range(N):
+        compare(from_dev(w_d[r]), w1, "f32", what=f"R50 bf16 w rank {r}")
+        off, ln = gdraa.gdraa_shard(N, r, L)
+        compare(from_dev(v_d[r])[off:off + ln], v1[off:off + ln], "f32", what=f"v rank {r}")
+
+
+@pytest.mark.parametrize("L", [synth.L_R50, synth.L_R101])
+def test_vr_full_size_fp32_n4(L):
+    """Configs 2/3 at full size (fp32, N=4 virtual ranks): every element."""
+    N = 4
+    gs = make_grads("like", 5, N, L, False)
+    w0, v0 = synth.w_like(5, L), synth.w_like(6, L)
+    w1, v1 = oracle.sgd_step(gs, w0, v0, synth.PAPER_LR, synth.PAPER_MOM)
+    g_d = [to_dev(g) for g in gs]
+    w_d = [to_dev(w0) for _ in range(N)]
+    v_d = [to_dev(v0) for _ in range(N)]
+    gdraa.gdraa_vr_sgd_step(w_d, g_d, v_d, synth.PAPER_LR, synth.PAPER_MOM)
+    torch.cuda.synchronize()
+    for r in range(N):
+        compare(from_dev(w_d[r]), w1, "f32", what=f"w rank {r}")
+        off, ln = gdraa.gdraa_shard(N, r, L)
+        compare(from_dev(v_d[r])[off:off + ln], v1[off:off + ln], "f32", what=f"v rank {r}")
+
+
+# ---------------------------------------------------------------------------------------
+# The multi-process ABI at world = 1 (init / register / sgd_step / allreduce / stats).
+# ---------------------------------------------------------------------------------------
+
+@pytest.fixture
+def world1():
+    gdraa.gdraa_init(1, 0)
+    yield
+    gdraa.gdraa_finalize()
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_world1_sgd_and_mean(world1, dt):
+    bf16 = dt == "bf16"
+    L = synth.L_R50
+    gs = make_grads("like", 8, 1, L, bf16)
+    w0, v0 = synth.w_like(8, L), synth.w_like(9, L)
+    g = to_dev(gs[0], bf16)
+    w, v = to_dev(w0), to_dev(v0)
+    gdraa.gdraa_register(w)
+    gdraa.gdraa_register(g)
+    for it in range(3):
+        w0, v0 = oracle.sgd_step(gs, w0, v0, synth.PAPER_LR, synth.PAPER_MOM)
+        gdraa.gdraa_sgd_step(w, g, v, synth.PAPER_LR, synth.PAPER_MOM)
+    torch.cuda.synchronize()
+    compare(from_dev(w), w0, "f32", what="w")
+    compare(from_dev(v), v0, "f32", what="v")
+    gdraa.gdraa_allreduce_mean(g)         # N = 1: identity, bit for bit
+    torch.cuda.synchronize()
+    assert np.array_equal(from_dev(g), gs[0])
+    st = gdraa.gdraa_get_stats()
+    assert st["calls"] == 4 and st["launches"] == 4 and st["sync_waits"] == 0, st
+
+
+def test_world1_errors(world1):
+    a = torch.zeros(1000, device=DEV)
+    b = torch.zeros(1000, device=DEV)
+    with pytest.raises(gdraa.GdraaError) as e:
+        gdraa.gdraa_sgd_step(a, b, a, 0.1, 0.9)
+    assert e.value.name == "GDRAA_ENOTREG"
+    gdraa.gdraa_register(a)
+    gdraa.gdraa_register(b)
+    with pytest.raises(gdraa.GdraaError) as e:
+        gdraa.gdraa_sgd_step(a, b, a, float("nan"), 0.9)
+    assert e.value.name == "GDRAA_EINVAL"
+    with pytest.raises(gdraa.GdraaError) as e:
+        gdraa.gdraa_register(a)
+    assert e.value.name == "GDRAA_EINVAL"
+    with pytest.raises(gdraa.GdraaError) as e:
+        gdraa.gdraa_register(a[1:], 999, gdraa.GDRAA_F32)       # misaligned
+    assert e.value.name == "GDRAA_EINVAL"
+    with pytest.raises(gdraa.GdraaError) as e:
+        gdraa.gdraa_init(1, 0)
+    assert e.value.name == "GDRAA_ESTATE"
+    c = torch.zeros(999, device=DEV)
+    gdraa.gdraa_register(c)
+    with pytest.raises(gdraa.GdraaError) as e:
+        gdraa.gdraa_sgd_step(a, c, b, 0.1, 0.9)                  # length mismatch
+    assert e.value.name == "GDRAA_EINVAL"
+
+
+def test_graph_capture_replays():
+    """The epoch lives in device memory, so a captured step replays correctly."""
+    N, L = 2, 100_003
+    gs = make_grads("like", 21, N, L, False)
+    w0, v0 = synth.w_like(21, L), np.zeros(L, np.float32)
+    g_d = [to_dev(g) for g in gs]
+    w_d = [to_dev(w0) for _ in range(N)]
+    v_d = [to_dev(v0) for _ in range(N)]
+    s = torch.cuda.Stream()
+    gdraa.gdraa_vr_sgd_step(w_d, g_d, v_d, 0.1, 0.9, stream=s)   # warm up (pads allocated)
+    s.synchronize()
+    w_ref, v_ref = oracle.sgd_step(gs, w0, v0, 0.1, 0.9)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        gdraa.gdraa_vr_sgd_step(w_d, g_d, v_d, 0.1, 0.9, stream=s)
+    for _ in range(3):
+        graph.replay()
+        w_ref, v_ref = oracle.sgd_step(gs, w_ref, v_ref, 0.1, 0.9)
+    torch.cuda.synchronize()
+    for r in range(N):
+        compare(from_dev(w_d[r]), w_ref, "f32", what=f"graph w rank {r}")

@@ -1,0 +1,96 @@
+"""Multi-process parity over NVLink: one process per GPU, job server control plane,
+CUDA-IPC peer mappings, the fused kernel pulling/pushing peer memory.  Runs with
+world = number of visible GPUs (2 or 4 under `gpurun --gpus N`); skipped on 1 GPU."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from tests.conftest import has_cuda
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu,
+              pytest.mark.skipif(not has_cuda() or torch.cuda.device_count() < 2,
+                                 reason="needs >= 2 GPUs")]
+
+
+def _worker(rank, world, sock, L_list, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    import synth
+    from paper_1802_02326_b200 import gdraa
+    from tests._parity import compare
+    from tests.test_gpu_parity import from_dev, make_grads, to_dev
+
+    torch.cuda.set_device(rank)
+    dev = f"cuda:{rank}"
+    os.environ["GDRAA_JOBSERVER"] = sock
+    gdraa.gdraa_init(world, rank)
+    report = {"rank": rank, "cases": 0}
+    calls = 0
+    for L in L_list:
+        for dt in ("f32", "bf16"):
+            bf16 = dt == "bf16"
+            for family in ("int", "like"):
+                gs = make_grads(family, 31 + L % 97, world, L, bf16)
+                # allreduce_mean (in place, registered buffer)
+                buf = to_dev(gs[rank], bf16, dev)
+                gdraa.gdraa_register(buf)
+                gdraa.gdraa_allreduce_mean(buf)
+                calls += 1
+                torch.cuda.synchronize()
+                compare(from_dev(buf), oracle.allreduce_mean(gs), dt,
+                        what=f"mean L={L} {dt} {family} rank {rank}")
+                # fused sgd_step, 3 chained iterations
+                if family == "int":
+                    w0, v0, lr, mom = (synth.w_integer(5, L), synth.v_integer(5, L),
+                                       synth.INT_LR, synth.INT_MOM)
+                else:
+                    w0, v0, lr, mom = (synth.w_like(5, L), np.zeros(L, np.float32),
+                                       synth.PAPER_LR, synth.PAPER_MOM)
+                g = to_dev(gs[rank], bf16, dev)
+                w, v = to_dev(w0, dev=dev), to_dev(v0, dev=dev)
+                gdraa.gdraa_register(w)
+                gdraa.gdraa_register(g)
+                off, ln = gdraa.gdraa_shard(world, rank, L)
+                for it in range(3 if family == "like" else 1):
+                    w0, v0 = oracle.sgd_step(gs, w0, v0, lr, mom)
+                    gdraa.gdraa_sgd_step(w, g, v, lr, mom)
+                    calls += 1
+                    torch.cuda.synchronize()
+                    compare(from_dev(w), w0, "f32", what=f"w it{it} L={L} {dt} {family} r{rank}")
+                    compare(from_dev(v)[off:off + ln], v0[off:off + ln], "f32",
+                            what=f"v it{it} L={L} {dt} {family} r{rank}")
+                assert np.array_equal(from_dev(g), gs[rank])     # g read-only (AMB-18)
+                for t in (buf, w, g):
+                    gdraa.gdraa_deregister(t)
+                report["cases"] += 1
+    st = gdraa.gdraa_get_stats()
+    assert st["calls"] == calls, (st, calls)
+    assert st["sync_waits"] == 2 * calls, st         # exactly two syncs per call
+    report["stats"] = st
+    gdraa.gdraa_finalize()
+    with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
+        json.dump(report, f)
+
+
+def test_multiprocess_parity(tmp_path):
+    from paper_1802_02326_b200 import jobserver
+    world = min(torch.cuda.device_count(), 8)
+    sock = str(tmp_path / "js.sock")
+    js = jobserver.start(world, sock)
+    L_list = [1, 1000, 70_001, 1 << 20]
+    try:
+        mp.start_processes(_worker, args=(world, sock, L_list, str(tmp_path)), nprocs=world,
+                           join=True, start_method="spawn")
+    finally:
+        out, err = js.communicate(timeout=120)
+    line = json.loads(out.strip().splitlines()[-1])["jobserver"]
+    assert line["ok"] and line["data_bytes"] == 0, line
+    assert line["ranks_joined"] == world
+    for r in range(world):
+        rep = json.load(open(tmp_path / f"rank{r}.json"))
+        assert rep["cases"] == len(L_list) * 4
