@@ -21,6 +21,8 @@ import time
 
 import numpy as np
 
+OUT = sys.stdout
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -122,50 +124,62 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------
 # the oracle as a CPU baseline (rank 0 only)
 # ---------------------------------------------------------------------------------------
-def oracle_sample_step(L, N, g_dt, budget_s):
-    """Time the CPU oracle (single-threaded C, as it stands) on a bounded sample of the
-    workload: the first n elements of every rank's buffer, n sized to ~budget_s total.
-    Returns (bytes/s in the metric's definition, sample description, seconds)."""
-    import oracle
-    n = min(L, 1 << 20)
-    gs = [synth.grad_like(0, p, n) for p in range(N)]
-    if g_dt == "bf16":
-        gs = [synth.to_bf16_bits_trunc(g) for g in gs]
-    w, v = synth.w_like(0, n), np.zeros(n, np.float32)
-    s_g = 2 if g_dt == "bf16" else 4
-    t0 = time.perf_counter()
-    oracle.sgd_step(gs, w, v, synth.PAPER_LR, synth.PAPER_MOM)
-    t1 = time.perf_counter() - t0
-    reps = max(1, int(budget_s / max(t1, 1e-6)))
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        w, v = oracle.sgd_step(gs, w, v, synth.PAPER_LR, synth.PAPER_MOM)
-    dt = (time.perf_counter() - t0) / reps
-    shard = [(n + N - 1) // N] * N
-    b = algorithmic_bytes(n, N, s_g, shard) * (N if N > 1 else 1)
-    return b / dt, (f"{reps} oracle steps over the first {n} elements of each of the {N} "
-                    f"rank buffers (of L={L})"), dt
+class OracleSample:
+    """The CPU oracle (single-threaded C, as it stands) on a bounded sample of the
+    workload: the first n elements of every one of the N rank buffers (all N ranks are
+    simulated in one process, as the oracle defines the method)."""
+
+    def __init__(self, L, N, g_dt, n=1 << 20):
+        import oracle
+        self.oracle, self.L, self.N, self.n = oracle, L, N, min(L, n)
+        self.gs = [synth.grad_like(0, p, self.n) for p in range(N)]
+        if g_dt == "bf16":
+            self.gs = [synth.to_bf16_bits_trunc(g) for g in self.gs]
+        self.w, self.v = synth.w_like(0, self.n), np.zeros(self.n, np.float32)
+        s_g = 2 if g_dt == "bf16" else 4
+        # the metric's bytes for this sample, summed over ranks as `value` is
+        self.bytes = algorithmic_bytes(self.n, N, s_g, None) * N
+
+    def step(self):
+        t0 = time.perf_counter()
+        self.w, self.v = self.oracle.sgd_step(self.gs, self.w, self.v, synth.PAPER_LR,
+                                              synth.PAPER_MOM)
+        return time.perf_counter() - t0
+
+    def describe(self, reps):
+        return (f"{reps} oracle sgd_step calls over the first {self.n} elements of each of "
+                f"the {self.N} rank buffers (L={self.L}); single thread")
+
+
+def oracle_baseline(L, N, g_dt, budget_s):
+    """(bytes/s, sample description, s/step) of the oracle over ~budget_s seconds."""
+    s = OracleSample(L, N, g_dt)
+    s.step()
+    reps, total = 0, 0.0
+    while total < budget_s:
+        total += s.step()
+        reps += 1
+    return s.bytes / (total / reps), s.describe(reps), total / reps
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle on the same config and metric."""
+    """--impl reference: the CPU oracle on the same config and metric.  Each step is one
+    oracle call over a bounded sample of the workload (OracleSample)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     L, g_dt, desc = CONFIGS[args.config]
     N = args.gpus
-    s_g = 2 if g_dt == "bf16" else 4
-    budget = 60.0 / max(1, args.steps + args.warmup)   # whole run within ~1 minute
-    vals = []
-    for i in range(args.warmup + args.steps):
-        v, sample, dt = oracle_sample_step(L, N, g_dt, budget)
-        if i >= args.warmup:
-            vals.append((v, dt))
-    value = float(np.mean([v for v, _ in vals])) / 1e9
+    s = OracleSample(L, N, g_dt)
+    for _ in range(args.warmup):
+        s.step()
+    dts = [s.step() for _ in range(args.steps)]
+    sample = s.describe(args.steps)
+    value = s.bytes / float(np.mean(dts)) / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
         "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": float(np.mean([d for _, d in vals])) * 1e3,
+        "ms_per_step": float(np.mean(dts)) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config_dict(args, L, g_dt, desc, N),
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
@@ -173,7 +187,7 @@ def run_reference(args):
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=OUT, flush=True)
     return 0
 
 
@@ -199,6 +213,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     args = ap.parse_args()
+    # Exactly one JSON line on stdout: anything libraries print (NCCL banners, ...) goes
+    # to stderr; the result line goes to the saved stdout.
+    global OUT
+    OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
@@ -339,7 +358,7 @@ def main():
         roof["kernel_ms"] = ms_step
         cpu = None
         if N == 1 and not args.no_cpu_baseline:
-            cv, sample, _ = oracle_sample_step(L, N, g_dt, 10.0)
+            cv, sample, _ = oracle_baseline(L, N, g_dt, 10.0)
             cpu = {"value": cv / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
                    "sample": sample}
         line = {
@@ -360,7 +379,7 @@ def main():
             "gpu_launches": launches, "clocks": clocks.summary() if clocks else None,
             "nccl_reference": nccl,
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=OUT, flush=True)
 
     barrier()
     gdraa.gdraa_finalize()

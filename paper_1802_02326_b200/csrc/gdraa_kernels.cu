@@ -11,11 +11,13 @@
 //   a7  exit barrier    = paper "1st synchronization" (Alg. 1)
 //
 // Rank r's CTAs read every peer's shard r through CUDA-IPC mapped pointers (coalesced
-// 128-bit loads, all N sources in flight per thread), and store the result shard to
-// all N ranks with 128-bit stores (posted NVLink writes).  Shard r is read and written
-// by rank r only, so in-place allreduce is race free chunk by chunk.  The rounding of
-// every operation is pinned (__fadd_rn / __fdiv_rn / __fmul_rn / __fsub_rn: never
-// contracted into FMA), so the result is bitwise that of the CPU oracle.
+// loads, all N sources in flight per thread), and store the result shard to all N
+// ranks with coalesced 128-bit stores (posted NVLink writes).  Every thread owns 4
+// consecutive elements per vector, so each warp-level load / store instruction covers
+// one contiguous span (256 B of bf16 g, 512 B of fp32 g/w/v): no partial-sector NVLink
+// writes.  Shard r is read and written by rank r only, so in-place allreduce is race
+// free chunk by chunk.  Every rounding is pinned (__fadd_rn / __fdiv_rn / __fmul_rn /
+// __fsub_rn are never contracted into FMA), so the result is bitwise the CPU oracle's.
 //
 // Tensor cores are not used: there is no contraction on this path.
 #include <cuda_bf16.h>
@@ -26,8 +28,6 @@
 
 namespace gdraa {
 namespace {
-
-constexpr int kThreads = 512;
 
 // ---------------------------------------------------------------------------------
 // PTX helpers
@@ -53,18 +53,28 @@ __device__ __forceinline__ uint64_t global_timer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-// Streaming 128-bit load: data is touched once, keep it out of L1.
-__device__ __forceinline__ uint4 ld_stream(const void *p) {
+// Streaming loads: data is touched once, keep it out of L1.
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
     uint4 r;
     asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
     return r;
 }
-__device__ __forceinline__ void st_v4(void *p, uint4 v) {
+__device__ __forceinline__ uint2 ld_stream(const uint2 *p) {
+    uint2 r;
+    asm volatile("ld.global.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                 : "=r"(r.x), "=r"(r.y)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_vec(uint4 *p, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
                  "r"(v.z), "r"(v.w)
                  : "memory");
+}
+__device__ __forceinline__ void st_vec(uint2 *p, uint2 v) {
+    asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
 }
 
 // Spin until *flag >= target, bounded by timeout_ns of %globaltimer.
@@ -89,18 +99,20 @@ __device__ __forceinline__ void report_timeout(ErrBlock *err, int phase, int pee
 }
 
 // ---------------------------------------------------------------------------------
-// Element access: 16 bytes of g per source per vector.
+// Element access: a vector is 4 consecutive elements; Raw is its storage in g / buf.
 // ---------------------------------------------------------------------------------
+constexpr int E = 4;
+
 template <typename TG> struct Elem;
 template <> struct Elem<float> {
-    static constexpr int E = 4;
-    __device__ __forceinline__ static void widen(uint4 r, float (&f)[E]) {
+    using Raw = uint4;                       // 16 bytes
+    __device__ __forceinline__ static void widen(Raw r, float (&f)[E]) {
         f[0] = __uint_as_float(r.x);
         f[1] = __uint_as_float(r.y);
         f[2] = __uint_as_float(r.z);
         f[3] = __uint_as_float(r.w);
     }
-    __device__ __forceinline__ static uint4 narrow(const float (&f)[E]) {
+    __device__ __forceinline__ static Raw narrow(const float (&f)[E]) {
         return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
                           __float_as_uint(f[3]));
     }
@@ -112,22 +124,23 @@ template <> struct Elem<float> {
     }
 };
 template <> struct Elem<__nv_bfloat16> {
-    static constexpr int E = 8;
+    using Raw = uint2;                       // 8 bytes
+    // bf16 -> fp32 is exact: the 16 bits become the high half (AMB-13).
     __device__ __forceinline__ static float lo(uint32_t u) { return __uint_as_float(u << 16); }
     __device__ __forceinline__ static float hi(uint32_t u) {
         return __uint_as_float(u & 0xFFFF0000u);
     }
-    __device__ __forceinline__ static void widen(uint4 r, float (&f)[E]) {
+    __device__ __forceinline__ static void widen(Raw r, float (&f)[E]) {
         f[0] = lo(r.x); f[1] = hi(r.x); f[2] = lo(r.y); f[3] = hi(r.y);
-        f[4] = lo(r.z); f[5] = hi(r.z); f[6] = lo(r.w); f[7] = hi(r.w);
     }
+    // fp32 -> bf16 round to nearest even (finite values).
     __device__ __forceinline__ static uint32_t pack(float a, float b) {
         const uint32_t l = __bfloat16_as_ushort(__float2bfloat16_rn(a));
         const uint32_t h = __bfloat16_as_ushort(__float2bfloat16_rn(b));
         return l | (h << 16);
     }
-    __device__ __forceinline__ static uint4 narrow(const float (&f)[E]) {
-        return make_uint4(pack(f[0], f[1]), pack(f[2], f[3]), pack(f[4], f[5]), pack(f[6], f[7]));
+    __device__ __forceinline__ static Raw narrow(const float (&f)[E]) {
+        return make_uint2(pack(f[0], f[1]), pack(f[2], f[3]));
     }
     __device__ __forceinline__ static float load1(const void *p, uint64_t i) {
         return lo(static_cast<const uint16_t *>(p)[i]);
@@ -154,15 +167,26 @@ __device__ __forceinline__ void sgd(float m, float lr, float mom, float &w, floa
     w = __fsub_rn(w, u);
 }
 
+__device__ __forceinline__ float4 ld_f4(const float *p) {
+    const uint4 r = ld_stream(reinterpret_cast<const uint4 *>(p));
+    return make_float4(__uint_as_float(r.x), __uint_as_float(r.y), __uint_as_float(r.z),
+                       __uint_as_float(r.w));
+}
+__device__ __forceinline__ uint4 as_u4(float a, float b, float c, float d) {
+    return make_uint4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(c),
+                      __float_as_uint(d));
+}
+
 // ---------------------------------------------------------------------------------
 // The fused kernel.  TG: gradient / buffer element type; WORLD: N; MODE: kMean or
-// kSgd; U: vectors per thread in flight per iteration (memory-level parallelism).
+// kSgd; U: vectors per thread in flight per iteration (memory-level parallelism);
+// THREADS x MINB: CTA size and minimum co-resident CTAs per SM (register budget).
 // ---------------------------------------------------------------------------------
-template <typename TG, int WORLD, int MODE, int U>
-__global__ void __launch_bounds__(kThreads)
+template <typename TG, int WORLD, int MODE, int U, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
 gdraa_kernel(const __grid_constant__ KParams p) {
     using EL = Elem<TG>;
-    constexpr int E = EL::E;
+    using Raw = typename EL::Raw;
     const int vr = blockIdx.y;
     const int rank = p.rank0 + vr;
     Pad *mine = p.pad[vr][rank];
@@ -194,85 +218,66 @@ gdraa_kernel(const __grid_constant__ KParams p) {
     const uint64_t off = min(static_cast<uint64_t>(rank) * p.blk, p.n);
     const uint64_t len = min(p.blk, p.n - off);
     const uint64_t nvec = len / E;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
-    uint64_t i = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * THREADS;
+    uint64_t i = static_cast<uint64_t>(blockIdx.x) * THREADS + threadIdx.x;
 
     const float lr = p.lr, mom = p.mom;
     float *const vloc = p.v[vr];
-    void *const wloc = p.dst[vr][rank];
+    const float *const wloc = static_cast<const float *>(p.dst[vr][rank]);
+    const Raw *src[WORLD];
+#pragma unroll
+    for (int q = 0; q < WORLD; ++q)
+        src[q] = reinterpret_cast<const Raw *>(static_cast<const TG *>(p.src[vr][q]) + off);
 
     auto process = [&](uint64_t i0, auto ucount) {
         constexpr int UU = decltype(ucount)::value;
-        uint4 raw[UU][WORLD];
-        float wv[UU][E], vv[UU][E];
+        Raw raw[UU][WORLD];
+        float4 wv[UU], vv[UU];
         // a3: reduce -- all N sources in flight at once (local HBM + N-1 NVLink peers).
 #pragma unroll
         for (int u = 0; u < UU; ++u) {
-            const uint64_t e0 = off + (i0 + u * stride) * E;
+            const uint64_t k = i0 + u * stride;
 #pragma unroll
-            for (int q = 0; q < WORLD; ++q)
-                raw[u][q] = ld_stream(static_cast<const TG *>(p.src[vr][q]) + e0);
+            for (int q = 0; q < WORLD; ++q) raw[u][q] = ld_stream(src[q] + k);
             if (MODE == kSgd) {
-#pragma unroll
-                for (int k = 0; k < E / 4; ++k) {
-                    const float4 a = *reinterpret_cast<const float4 *>(
-                        static_cast<const float *>(wloc) + e0 + 4 * k);
-                    const float4 b = *reinterpret_cast<const float4 *>(vloc + e0 + 4 * k);
-                    wv[u][4 * k + 0] = a.x; wv[u][4 * k + 1] = a.y;
-                    wv[u][4 * k + 2] = a.z; wv[u][4 * k + 3] = a.w;
-                    vv[u][4 * k + 0] = b.x; vv[u][4 * k + 1] = b.y;
-                    vv[u][4 * k + 2] = b.z; vv[u][4 * k + 3] = b.w;
-                }
+                wv[u] = ld_f4(wloc + off + k * E);
+                vv[u] = ld_f4(vloc + off + k * E);
             }
         }
-        // a4 (+ a5): aggregate (and update) in registers.
-        float out[UU][E];
+        // a4 (+ a5): aggregate (and update) in registers; a6: push to every rank.
 #pragma unroll
         for (int u = 0; u < UU; ++u) {
+            const uint64_t e0 = off + (i0 + u * stride) * E;
             float x[WORLD][E];
 #pragma unroll
             for (int q = 0; q < WORLD; ++q) EL::widen(raw[u][q], x[q]);
+            float m[E];
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 float col[WORLD];
 #pragma unroll
                 for (int q = 0; q < WORLD; ++q) col[q] = x[q][e];
-                const float m = average<WORLD>(col);
-                if (MODE == kSgd) {
-                    sgd(m, lr, mom, wv[u][e], vv[u][e]);
-                    out[u][e] = wv[u][e];
-                } else {
-                    out[u][e] = m;
-                }
+                m[e] = average<WORLD>(col);
             }
-        }
-        // a6: broadcast -- push the block to every rank (own copy last).
-#pragma unroll
-        for (int u = 0; u < UU; ++u) {
-            const uint64_t e0 = off + (i0 + u * stride) * E;
             if (MODE == kSgd) {
+                float4 w = wv[u], v = vv[u];
+                sgd(m[0], lr, mom, w.x, v.x);
+                sgd(m[1], lr, mom, w.y, v.y);
+                sgd(m[2], lr, mom, w.z, v.z);
+                sgd(m[3], lr, mom, w.w, v.w);
+                st_vec(reinterpret_cast<uint4 *>(vloc + e0), as_u4(v.x, v.y, v.z, v.w));
+                const uint4 o = as_u4(w.x, w.y, w.z, w.w);
 #pragma unroll
-                for (int k = 0; k < E / 4; ++k)
-                    *reinterpret_cast<float4 *>(vloc + e0 + 4 * k) =
-                        make_float4(vv[u][4 * k], vv[u][4 * k + 1], vv[u][4 * k + 2],
-                                    vv[u][4 * k + 3]);
-#pragma unroll
-                for (int k = 0; k < E / 4; ++k) {
-                    const uint4 o = make_uint4(
-                        __float_as_uint(out[u][4 * k]), __float_as_uint(out[u][4 * k + 1]),
-                        __float_as_uint(out[u][4 * k + 2]), __float_as_uint(out[u][4 * k + 3]));
-#pragma unroll
-                    for (int j = 1; j <= WORLD; ++j) {
-                        const int q = (rank + j) % WORLD;
-                        st_v4(static_cast<float *>(p.dst[vr][q]) + e0 + 4 * k, o);
-                    }
+                for (int j = 1; j <= WORLD; ++j) {   // own copy last
+                    const int q = (rank + j) % WORLD;
+                    st_vec(reinterpret_cast<uint4 *>(static_cast<float *>(p.dst[vr][q]) + e0), o);
                 }
             } else {
-                const uint4 o = EL::narrow(out[u]);
+                const Raw o = EL::narrow(m);
 #pragma unroll
                 for (int j = 1; j <= WORLD; ++j) {
                     const int q = (rank + j) % WORLD;
-                    st_v4(static_cast<TG *>(p.dst[vr][q]) + e0, o);
+                    st_vec(reinterpret_cast<Raw *>(static_cast<TG *>(p.dst[vr][q]) + e0), o);
                 }
             }
         }
@@ -284,16 +289,16 @@ gdraa_kernel(const __grid_constant__ KParams p) {
     }
     for (; i < nvec; i += stride) process(i, std::integral_constant<int, 1>{});
 
-    // Ragged tail of the last non-empty shard (len % E elements), scalar.
+    // Ragged tail of the last non-empty shard (len % 4 elements), scalar.
     if (blockIdx.x == gridDim.x - 1) {
-        for (uint64_t t = nvec * E + threadIdx.x; t < len; t += kThreads) {
+        for (uint64_t t = nvec * E + threadIdx.x; t < len; t += THREADS) {
             const uint64_t e = off + t;
             float col[WORLD];
 #pragma unroll
             for (int q = 0; q < WORLD; ++q) col[q] = EL::load1(p.src[vr][q], e);
             const float m = average<WORLD>(col);
             if (MODE == kSgd) {
-                float w = static_cast<const float *>(wloc)[e], v = vloc[e];
+                float w = wloc[e], v = vloc[e];
                 sgd(m, lr, mom, w, v);
                 vloc[e] = v;
                 for (int j = 1; j <= WORLD; ++j)
@@ -306,7 +311,7 @@ gdraa_kernel(const __grid_constant__ KParams p) {
 
     // a7: "1st synchronization" -- our pushes are performed system-wide, then the last
     // CTA of this rank tells every peer and waits until every peer has done the same.
-    fence_acq_rel_sys();
+    if (WORLD > 1) fence_acq_rel_sys();   // N = 1: the kernel boundary orders our stores
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned prev = atomicAdd(&mine->arrive, 1u);
@@ -337,21 +342,34 @@ gdraa_kernel(const __grid_constant__ KParams p) {
 }
 
 // ---------------------------------------------------------------------------------
-// Dispatch
+// Launch shapes (measured on B200): vectors in flight per
+// thread U, CTA size and CTAs per SM.
 // ---------------------------------------------------------------------------------
-// Vectors in flight per thread: enough 16-byte loads to cover NVLink latency without
-// spilling (bf16 vectors expand to 8 fp32 values each, so they get half the depth).
-template <typename TG, int WORLD> constexpr int unroll_for() {
-    return sizeof(TG) == 4 ? (WORLD <= 2 ? 4 : (WORLD <= 4 ? 2 : 1)) : (WORLD <= 2 ? 2 : 1);
-}
+// N <= 2 (profiles/r04_tune*.jsonl): 1024 threads x U=2 is the best or within 1% of it
+// for both dtypes and modes (N=1 sgd 87.9 us vs 97.6 us for 512 x U=4; N=2 sgd 174.0 us).
+// N >= 3 keeps 512 threads: its register need (N sources in flight) exceeds the 64 a
+// 1024-thread CTA allows.
+template <typename TG, int WORLD, int MODE> struct Shape {
+    static constexpr int U = WORLD <= 4 ? 2 : 1;
+    static constexpr int THREADS = WORLD <= 2 ? 1024 : 512;
+    static constexpr int MINB = 1;
+};
 
 using KernelFn = void (*)(KParams);
 
+struct Launch {
+    KernelFn fn;
+    int threads;
+};
+
 template <typename TG, int MODE, int WORLD>
-KernelFn pick_w() { return gdraa_kernel<TG, WORLD, MODE, unroll_for<TG, WORLD>()>; }
+Launch pick_w() {
+    using S = Shape<TG, WORLD, MODE>;
+    return {gdraa_kernel<TG, WORLD, MODE, S::U, S::THREADS, S::MINB>, S::THREADS};
+}
 
 template <typename TG, int MODE>
-KernelFn pick_m(int world) {
+Launch pick_m(int world) {
     switch (world) {
         case 1: return pick_w<TG, MODE, 1>();
         case 2: return pick_w<TG, MODE, 2>();
@@ -361,11 +379,11 @@ KernelFn pick_m(int world) {
         case 6: return pick_w<TG, MODE, 6>();
         case 7: return pick_w<TG, MODE, 7>();
         case 8: return pick_w<TG, MODE, 8>();
-        default: return nullptr;
+        default: return {nullptr, 0};
     }
 }
 
-KernelFn pick(int dtype, int mode, int world) {
+Launch pick(int dtype, int mode, int world) {
     if (dtype == GDRAA_F32)
         return mode == kSgd ? pick_m<float, kSgd>(world) : pick_m<float, kMean>(world);
     return mode == kSgd ? pick_m<__nv_bfloat16, kSgd>(world) : pick_m<__nv_bfloat16, kMean>(world);
@@ -374,35 +392,43 @@ KernelFn pick(int dtype, int mode, int world) {
 }  // namespace
 
 int max_ctas(int dtype, int mode, int world) {
-    KernelFn fn = pick(dtype, mode, world);
-    if (fn == nullptr) return 0;
-    int dev = 0, sms = 0, per_sm = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0) != cudaSuccess)
-        return 0;
-    return sms * per_sm;
+    Launch l = pick(dtype, mode, world);
+    if (l.fn == nullptr) return 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+    // co-resident CTAs per device and kernel, queried once (it is on the launch path)
+    static int cache[64][2][2][kMaxWorld + 1];
+    int &c = cache[dev][dtype == GDRAA_F32 ? 0 : 1][mode == kSgd ? 1 : 0][world];
+    if (c == 0) {
+        int sms = 0, per_sm = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            return 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l.fn, l.threads, 0) !=
+            cudaSuccess)
+            return 0;
+        c = sms * per_sm;
+    }
+    return c;
 }
 
 cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows, bool cooperative,
                          cudaStream_t s, int *grid_x_out) {
-    KernelFn fn = pick(dtype, mode, p.world);
-    if (fn == nullptr) return cudaErrorInvalidValue;
+    Launch l = pick(dtype, mode, p.world);
+    if (l.fn == nullptr) return cudaErrorInvalidValue;
     const int cap = max_ctas(dtype, mode, p.world) / vr_rows;
     if (cap < 1) return cudaErrorInvalidConfiguration;
-    const int E = dtype == GDRAA_F32 ? 4 : 8;
     const uint64_t nvec = (p.blk + E - 1) / E;
-    const uint64_t want = (nvec + kThreads - 1) / kThreads;
+    const uint64_t want = (nvec + l.threads - 1) / l.threads;
     int gx = static_cast<int>(want < static_cast<uint64_t>(cap) ? want : cap);
     if (gx < 1) gx = 1;
     if (grid_x_out) *grid_x_out = gx;
-    dim3 grid(gx, vr_rows), block(kThreads);
+    dim3 grid(gx, vr_rows), block(l.threads);
     if (cooperative) {
         void *args[] = {const_cast<KParams *>(&p)};
-        return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(fn), grid, block, args,
-                                           0, s);
+        return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(l.fn), grid, block,
+                                           args, 0, s);
     }
-    fn<<<grid, block, 0, s>>>(p);
+    l.fn<<<grid, block, 0, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,192 @@
+// tune.cu -- launch-shape sweep of the GDRAA kernel on 1..4 B200s of one box, single
+// process: rank d's kernel runs on device d and reaches its peers through
+// cudaDeviceEnablePeerAccess pointers (same kernel code as the library; the IPC and job
+// server plumbing is not involved).  Prints one JSON line per (shape, config).
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
+//        -o tools/tune tools/tune.cu
+//   ./tools/tune <world> <L> <f32|bf16> <sgd|mean> [iters]
+#include "../paper_1802_02326_b200/csrc/gdraa_kernels.cu"
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace gdraa;
+
+#define CK(x)                                                                            \
+    do {                                                                                 \
+        cudaError_t e = (x);                                                             \
+        if (e != cudaSuccess) {                                                          \
+            std::fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x,               \
+                         cudaGetErrorString(e));                                         \
+            std::exit(1);                                                                \
+        }                                                                                \
+    } while (0)
+
+struct Bufs {
+    void *g[3];
+    float *w[3], *v[3];
+    Pad *pad;
+};
+
+static int W, NDEV;
+static size_t L;
+static int DT, MODE_;
+static int ITERS = 50;
+static std::vector<Bufs> B;
+static ErrBlock *err_d;
+
+template <typename TG, int WORLD, int MODE, int U, int THREADS, int MINB>
+void run_shape(int grid_div) {
+    auto fn = gdraa_kernel<TG, WORLD, MODE, U, THREADS, MINB>;
+    int sms = 0, per = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, THREADS, 0));
+    uint64_t blk, off, len;
+    {
+        const uint64_t c = (L + WORLD - 1) / WORLD;
+        blk = (c + kQuantum - 1) / kQuantum * kQuantum;
+        (void)off; (void)len;
+    }
+    const uint64_t nvec = (blk + 3) / 4;
+    uint64_t want = (nvec + THREADS - 1) / THREADS;
+    int gx = (int)std::min<uint64_t>(want, (uint64_t)sms * per / grid_div);
+    if (gx < 1) gx = 1;
+    std::vector<cudaStream_t> st(WORLD);
+    std::vector<cudaEvent_t> e0(WORLD), e1(WORLD);
+    for (int d = 0; d < WORLD; ++d) {
+        CK(cudaSetDevice(d));
+        CK(cudaStreamCreate(&st[d]));
+        CK(cudaEventCreate(&e0[d]));
+        CK(cudaEventCreate(&e1[d]));
+    }
+    auto launch = [&](int set) {
+        for (int d = 0; d < WORLD; ++d) {
+            KParams p;
+            std::memset(&p, 0, sizeof p);
+            p.world = WORLD;
+            p.rank0 = d;
+            p.n = L;
+            p.blk = blk;
+            p.lr = 0.1f;
+            p.mom = 0.9f;
+            p.timeout_ns = 10ull * 1000000000ull;
+            for (int q = 0; q < WORLD; ++q) {
+                p.src[0][q] = B[q].g[set];
+                p.dst[0][q] = MODE == kSgd ? (void *)B[q].w[set] : B[q].g[set];
+                p.pad[0][q] = B[q].pad;
+            }
+            p.v[0] = B[d].v[set];
+            p.err = err_d;
+            CK(cudaSetDevice(d));
+            fn<<<dim3(gx, 1), THREADS, 0, st[d]>>>(p);
+            CK(cudaGetLastError());
+        }
+    };
+    for (int i = 0; i < 5; ++i) launch(i % 3);
+    for (int d = 0; d < WORLD; ++d) { CK(cudaSetDevice(d)); CK(cudaDeviceSynchronize()); }
+    for (int d = 0; d < WORLD; ++d) { CK(cudaSetDevice(d)); CK(cudaEventRecord(e0[d], st[d])); }
+    for (int i = 0; i < ITERS; ++i) launch(i % 3);
+    float worst = 0;
+    for (int d = 0; d < WORLD; ++d) {
+        CK(cudaSetDevice(d));
+        CK(cudaEventRecord(e1[d], st[d]));
+        CK(cudaEventSynchronize(e1[d]));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0[d], e1[d]));
+        worst = std::max(worst, ms);
+    }
+    if (err_d->code) {
+        std::fprintf(stderr, "timeout reported\n");
+        std::exit(2);
+    }
+    const double t = worst / ITERS * 1e-3;
+    const int sg = sizeof(TG);
+    double bytes = WORLD == 1 ? (MODE == kSgd ? (sg + 16.0) * L : 2.0 * sg * L)
+                              : (WORLD - 1.0) / WORLD * L * (sg + (MODE == kSgd ? 4 : sg));
+    std::printf("{\"world\": %d, \"L\": %zu, \"dtype\": \"%s\", \"mode\": \"%s\", \"U\": %d, "
+                "\"threads\": %d, \"minb\": %d, \"per_sm\": %d, \"grid\": %d, \"us\": %.2f, "
+                "\"gbs_per_rank\": %.1f}\n",
+                WORLD, L, sg == 4 ? "f32" : "bf16", MODE == kSgd ? "sgd" : "mean", U, THREADS,
+                MINB, per, gx, t * 1e6, bytes / t / 1e9);
+    std::fflush(stdout);
+    for (int d = 0; d < WORLD; ++d) {
+        CK(cudaSetDevice(d));
+        CK(cudaStreamDestroy(st[d]));
+    }
+}
+
+template <typename TG, int WORLD, int MODE>
+void sweep() {
+    run_shape<TG, WORLD, MODE, 1, 512, 1>(1);
+    run_shape<TG, WORLD, MODE, 2, 512, 1>(1);
+    run_shape<TG, WORLD, MODE, 4, 512, 1>(1);
+    run_shape<TG, WORLD, MODE, 1, 256, 1>(1);
+    run_shape<TG, WORLD, MODE, 2, 256, 1>(1);
+    run_shape<TG, WORLD, MODE, 4, 256, 1>(1);
+    run_shape<TG, WORLD, MODE, 1, 512, 2>(1);
+    run_shape<TG, WORLD, MODE, 2, 512, 2>(1);
+    run_shape<TG, WORLD, MODE, 1, 1024, 1>(1);
+    run_shape<TG, WORLD, MODE, 2, 1024, 1>(1);
+    run_shape<TG, WORLD, MODE, 8, 256, 1>(1);
+    run_shape<TG, WORLD, MODE, 2, 512, 1>(2);
+    run_shape<TG, WORLD, MODE, 4, 256, 1>(2);
+}
+
+template <typename TG, int MODE>
+void dispatch_world() {
+    switch (W) {
+        case 1: sweep<TG, 1, MODE>(); break;
+        case 2: sweep<TG, 2, MODE>(); break;
+        case 4: sweep<TG, 4, MODE>(); break;
+        default: std::fprintf(stderr, "world must be 1, 2 or 4\n"); std::exit(1);
+    }
+}
+
+int main(int argc, char **argv) {
+    if (argc < 5) {
+        std::fprintf(stderr, "usage: tune <world> <L> <f32|bf16> <sgd|mean> [iters]\n");
+        return 1;
+    }
+    W = std::atoi(argv[1]);
+    L = std::strtoull(argv[2], nullptr, 10);
+    DT = std::string(argv[3]) == "bf16" ? GDRAA_BF16 : GDRAA_F32;
+    MODE_ = std::string(argv[4]) == "mean" ? kMean : kSgd;
+    if (argc > 5) ITERS = std::atoi(argv[5]);
+    CK(cudaGetDeviceCount(&NDEV));
+    if (NDEV < W) {
+        std::fprintf(stderr, "need %d GPUs, have %d\n", W, NDEV);
+        return 1;
+    }
+    const size_t gb = L * (DT == GDRAA_BF16 ? 2 : 4);
+    B.resize(W);
+    for (int d = 0; d < W; ++d) {
+        CK(cudaSetDevice(d));
+        for (int q = 0; q < W; ++q)
+            if (q != d) CK(cudaDeviceEnablePeerAccess(q, 0));
+        for (int s = 0; s < 3; ++s) {
+            CK(cudaMalloc(&B[d].g[s], gb));
+            CK(cudaMalloc(&B[d].w[s], L * 4));
+            CK(cudaMalloc(&B[d].v[s], L * 4));
+            CK(cudaMemset(B[d].g[s], 0, gb));
+            CK(cudaMemset(B[d].w[s], 0, L * 4));
+            CK(cudaMemset(B[d].v[s], 0, L * 4));
+        }
+        CK(cudaMalloc(&B[d].pad, sizeof(Pad)));
+        CK(cudaMemset(B[d].pad, 0, sizeof(Pad)));
+    }
+    void *eh;
+    CK(cudaHostAlloc(&eh, sizeof(ErrBlock), cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(eh, 0, sizeof(ErrBlock));
+    CK(cudaHostGetDevicePointer((void **)&err_d, eh, 0));
+    err_d = (ErrBlock *)eh;   // UVA: host pointer valid on device
+    if (DT == GDRAA_F32) {
+        if (MODE_ == kSgd) dispatch_world<float, kSgd>(); else dispatch_world<float, kMean>();
+    } else {
+        if (MODE_ == kSgd) dispatch_world<__nv_bfloat16, kSgd>(); else dispatch_world<__nv_bfloat16, kMean>();
+    }
+    return 0;
+}
