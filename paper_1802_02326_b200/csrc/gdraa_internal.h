@@ -26,7 +26,7 @@ struct alignas(128) Pad {
     uint64_t calls;
     uint64_t sync_waits;
     uint32_t arrive;               // CTA arrival counter of the running call
-    uint32_t _p2;
+    uint32_t next;                 // next work chunk of the running call (dynamic schedule)
     uint64_t _p3[12];
 };
 static_assert(sizeof(Pad) % 128 == 0, "pad layout");
@@ -55,6 +55,9 @@ struct KParams {
     Pad *pad[kMaxWorld][kMaxWorld];          // [vr][p]: rank p's pad seen from vr
     ErrBlock *err;                           // host-mapped (device alias)
     volatile uint64_t *done[kMaxWorld];      // host-mapped done flags (device alias) or null
+#ifdef GDRAA_TRACE
+    uint64_t *trace;                         // tools/tune.cu only: %globaltimer stamps
+#endif
 };
 
 enum Mode { kMean = 0, kSgd = 1 };

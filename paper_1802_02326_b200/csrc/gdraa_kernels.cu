@@ -98,6 +98,18 @@ __device__ __forceinline__ void report_timeout(ErrBlock *err, int phase, int pee
     err->code = GDRAA_ETIMEOUT;
 }
 
+// Phase timestamps for tools/tune.cu (compiled out of the library).
+#ifdef GDRAA_TRACE
+#define GDRAA_STAMP(k)                                                                   \
+    do {                                                                                 \
+        if (p.trace) p.trace[((epoch % 64) * kMaxWorld + vr) * 8 + (k)] = global_timer_ns(); \
+    } while (0)
+#else
+#define GDRAA_STAMP(k) \
+    do {               \
+    } while (0)
+#endif
+
 // ---------------------------------------------------------------------------------
 // Element access: a vector is 4 consecutive elements; Raw is its storage in g / buf.
 // ---------------------------------------------------------------------------------
@@ -197,6 +209,7 @@ gdraa_kernel(const __grid_constant__ KParams p) {
     // last CTA updates it only after every CTA arrived: one consistent value per call.
     const uint64_t epoch = *reinterpret_cast<volatile uint64_t *>(&mine->epoch) + 1;
     if (threadIdx.x == 0) s_abort = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(0);
 
     // a2: "2nd synchronization" -- every peer's D(i) is final (stream-ordered after its
     // backward) before anyone reads it or writes into it.
@@ -213,13 +226,12 @@ gdraa_kernel(const __grid_constant__ KParams p) {
         __syncthreads();
         if (s_abort) return;
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(1);
 
     // a1: this rank's block D(., r), Q-aligned ceil partition (AMB-8).
     const uint64_t off = min(static_cast<uint64_t>(rank) * p.blk, p.n);
     const uint64_t len = min(p.blk, p.n - off);
     const uint64_t nvec = len / E;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * THREADS;
-    uint64_t i = static_cast<uint64_t>(blockIdx.x) * THREADS + threadIdx.x;
 
     const float lr = p.lr, mom = p.mom;
     float *const vloc = p.v[vr];
@@ -229,14 +241,15 @@ gdraa_kernel(const __grid_constant__ KParams p) {
     for (int q = 0; q < WORLD; ++q)
         src[q] = reinterpret_cast<const Raw *>(static_cast<const TG *>(p.src[vr][q]) + off);
 
-    auto process = [&](uint64_t i0, auto ucount) {
+    // Vectors k0, k0 + THREADS, ..., k0 + (UU-1) * THREADS of the shard.
+    auto process = [&](uint64_t k0, auto ucount) {
         constexpr int UU = decltype(ucount)::value;
         Raw raw[UU][WORLD];
         float4 wv[UU], vv[UU];
         // a3: reduce -- all N sources in flight at once (local HBM + N-1 NVLink peers).
 #pragma unroll
         for (int u = 0; u < UU; ++u) {
-            const uint64_t k = i0 + u * stride;
+            const uint64_t k = k0 + u * THREADS;
 #pragma unroll
             for (int q = 0; q < WORLD; ++q) raw[u][q] = ld_stream(src[q] + k);
             if (MODE == kSgd) {
@@ -247,7 +260,7 @@ gdraa_kernel(const __grid_constant__ KParams p) {
         // a4 (+ a5): aggregate (and update) in registers; a6: push to every rank.
 #pragma unroll
         for (int u = 0; u < UU; ++u) {
-            const uint64_t e0 = off + (i0 + u * stride) * E;
+            const uint64_t e0 = off + (k0 + u * THREADS) * E;
             float x[WORLD][E];
 #pragma unroll
             for (int q = 0; q < WORLD; ++q) EL::widen(raw[u][q], x[q]);
@@ -283,11 +296,33 @@ gdraa_kernel(const __grid_constant__ KParams p) {
         }
     };
 
-    if (U > 1) {
-        for (; i + (U - 1) * stride < nvec; i += U * stride)
-            process(i, std::integral_constant<int, U>{});
+    // Dynamic schedule: CTAs take chunks from a per-rank counter (the next index is
+    // fetched while the current chunk is in flight).  A static grid-stride split left
+    // the slowest CTA finishing 41 us after CTA 0 at R50 / N=2 (profiles/r07_trace_n2).
+    // Big chunks (THREADS*U vectors) first; the last ~2 waves use THREADS-vector chunks
+    // so the CTAs finish close together.
+    const uint64_t big = static_cast<uint64_t>(THREADS) * U;
+    const uint64_t tailv = 2ull * gridDim.x * THREADS;
+    const uint64_t nbig = nvec > tailv ? (nvec - tailv) / big : 0;
+    const uint64_t small0 = nbig * big;
+    const uint64_t nchunks = nbig + (nvec - small0 + THREADS - 1) / THREADS;
+    __shared__ uint32_t s_chunk[2];
+    if (threadIdx.x == 0) s_chunk[0] = atomicAdd(&mine->next, 1u);
+    __syncthreads();
+    uint32_t c = s_chunk[0];
+    int slot = 0;
+    while (c < nchunks) {
+        if (threadIdx.x == 0) s_chunk[slot ^ 1] = atomicAdd(&mine->next, 1u);
+        if (c < nbig) {
+            process(c * big + threadIdx.x, std::integral_constant<int, U>{});
+        } else {
+            const uint64_t k = small0 + (c - nbig) * THREADS + threadIdx.x;
+            if (k < nvec) process(k, std::integral_constant<int, 1>{});
+        }
+        __syncthreads();
+        c = s_chunk[slot ^ 1];
+        slot ^= 1;
     }
-    for (; i < nvec; i += stride) process(i, std::integral_constant<int, 1>{});
 
     // Ragged tail of the last non-empty shard (len % 4 elements), scalar.
     if (blockIdx.x == gridDim.x - 1) {
@@ -311,6 +346,7 @@ gdraa_kernel(const __grid_constant__ KParams p) {
 
     // a7: "1st synchronization" -- our pushes are performed system-wide, then the last
     // CTA of this rank tells every peer and waits until every peer has done the same.
+    if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(2);
     if (WORLD > 1) fence_acq_rel_sys();   // N = 1: the kernel boundary orders our stores
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -320,6 +356,7 @@ gdraa_kernel(const __grid_constant__ KParams p) {
     }
     __syncthreads();
     if (!s_last) return;
+    if (threadIdx.x == 0) GDRAA_STAMP(3);
     if (WORLD > 1) {
         if (threadIdx.x < WORLD && threadIdx.x != rank)
             st_release_sys(&p.pad[vr][threadIdx.x]->exit[rank], epoch);
@@ -333,7 +370,9 @@ gdraa_kernel(const __grid_constant__ KParams p) {
         if (s_abort) return;
     }
     if (threadIdx.x == 0) {
+        GDRAA_STAMP(4);
         mine->arrive = 0;
+        mine->next = 0;
         mine->calls += 1;
         if (WORLD > 1) mine->sync_waits += 2;
         mine->epoch = epoch;
@@ -347,12 +386,15 @@ gdraa_kernel(const __grid_constant__ KParams p) {
 // ---------------------------------------------------------------------------------
 // N <= 2 (profiles/r04_tune*.jsonl): 1024 threads x U=2 is the best or within 1% of it
 // for both dtypes and modes (N=1 sgd 87.9 us vs 97.6 us for 512 x U=4; N=2 sgd 174.0 us).
-// N >= 3 keeps 512 threads: its register need (N sources in flight) exceeds the 64 a
-// 1024-thread CTA allows.
+// N = 4 (profiles/r06_tune_n4.jsonl): 2 CTAs x 512 threads x U=2 is best for all four
+// (f32 sgd 247.9 us vs 252.5 us at 1 CTA/SM).  N > 4 keeps 2 x 512 with U=1 so that N
+// sources in flight still fit the 64 registers of two 512-thread CTAs per SM.
+// N = 1 with the dynamic schedule (profiles/r09_tune_n1.jsonl): 2 x 512 threads, U=1 is
+// best (84.1 us = 6081 GB/s vs 88.2 us for 1024 x U=2).
 template <typename TG, int WORLD, int MODE> struct Shape {
-    static constexpr int U = WORLD <= 4 ? 2 : 1;
-    static constexpr int THREADS = WORLD <= 2 ? 1024 : 512;
-    static constexpr int MINB = 1;
+    static constexpr int U = WORLD == 1 ? 1 : (WORLD <= 4 ? 2 : 1);
+    static constexpr int THREADS = WORLD == 2 ? 1024 : 512;
+    static constexpr int MINB = WORLD == 2 ? 1 : 2;
 };
 
 using KernelFn = void (*)(KParams);
@@ -360,12 +402,13 @@ using KernelFn = void (*)(KParams);
 struct Launch {
     KernelFn fn;
     int threads;
+    int u;
 };
 
 template <typename TG, int MODE, int WORLD>
 Launch pick_w() {
     using S = Shape<TG, WORLD, MODE>;
-    return {gdraa_kernel<TG, WORLD, MODE, S::U, S::THREADS, S::MINB>, S::THREADS};
+    return {gdraa_kernel<TG, WORLD, MODE, S::U, S::THREADS, S::MINB>, S::THREADS, S::U};
 }
 
 template <typename TG, int MODE>
@@ -379,7 +422,7 @@ Launch pick_m(int world) {
         case 6: return pick_w<TG, MODE, 6>();
         case 7: return pick_w<TG, MODE, 7>();
         case 8: return pick_w<TG, MODE, 8>();
-        default: return {nullptr, 0};
+        default: return {nullptr, 0, 0};
     }
 }
 
@@ -418,7 +461,8 @@ cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows, boo
     const int cap = max_ctas(dtype, mode, p.world) / vr_rows;
     if (cap < 1) return cudaErrorInvalidConfiguration;
     const uint64_t nvec = (p.blk + E - 1) / E;
-    const uint64_t want = (nvec + l.threads - 1) / l.threads;
+    const uint64_t per_chunk = static_cast<uint64_t>(l.threads) * l.u;
+    const uint64_t want = (nvec + per_chunk - 1) / per_chunk;   // chunks of the largest shard
     int gx = static_cast<int>(want < static_cast<uint64_t>(cap) ? want : cap);
     if (gx < 1) gx = 1;
     if (grid_x_out) *grid_x_out = gx;

@@ -44,6 +44,37 @@ __global__ void copy_kernel(const uint4 *__restrict__ src, uint4 *__restrict__ d
     for (; i < n; i += stride) dst[i] = ldg_na(src + i);
 }
 
+// 256-bit variant (sm_100 LDG.E.ENL2.256 / STG.E.ENL2.256): 32 bytes per thread.
+struct alignas(32) V8 {
+    uint32_t a[8];
+};
+__device__ __forceinline__ V8 ld8(const V8 *p) {
+    V8 r;
+    asm volatile("ld.global.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.a[0]), "=r"(r.a[1]), "=r"(r.a[2]), "=r"(r.a[3]), "=r"(r.a[4]),
+                   "=r"(r.a[5]), "=r"(r.a[6]), "=r"(r.a[7])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st8(V8 *p, const V8 &v) {
+    asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.a[0]),
+                 "r"(v.a[1]), "r"(v.a[2]), "r"(v.a[3]), "r"(v.a[4]), "r"(v.a[5]), "r"(v.a[6]),
+                 "r"(v.a[7])
+                 : "memory");
+}
+template <int U>
+__global__ void copy8_kernel(const V8 *__restrict__ src, V8 *__restrict__ dst, size_t n) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (U - 1) * stride < n; i += U * stride) {
+        V8 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ld8(src + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < U; ++u) st8(dst + i + u * stride, v[u]);
+    }
+}
+
 // sum of two sources (one remote) into dst (the pull-reduce of the current kernel).
 template <int U>
 __global__ void pull_reduce_push(const uint4 *__restrict__ local, const uint4 *__restrict__ remote,
@@ -272,6 +303,40 @@ int main(int argc, char **argv) {
                     copy_kernel<4><<<g_sms * grid_mult, 512, 0, s>>>((const uint4 *)p.buf[d][0], (uint4 *)p.buf[1 - d][2], n16);
             });
         }
+    // 256-bit pull / push
+    for (int grid_mult : {1, 2}) {
+        char name[64];
+        std::snprintf(name, sizeof name, "pull_v8_u2_g%d", grid_mult);
+        run_bidir(name, bytes, [&](int d, cudaStream_t s) {
+            copy8_kernel<2><<<g_sms * grid_mult, 512, 0, s>>>((const V8 *)p.buf[1 - d][0], (V8 *)p.buf[d][1], bytes / 32);
+        });
+        std::snprintf(name, sizeof name, "push_v8_u2_g%d", grid_mult);
+        run_bidir(name, bytes, [&](int d, cudaStream_t s) {
+            copy8_kernel<2><<<g_sms * grid_mult, 512, 0, s>>>((const V8 *)p.buf[d][0], (V8 *)p.buf[1 - d][2], bytes / 32);
+        });
+    }
+    // one-directional references (only device 0 moves data)
+    {
+        auto one = [&](const char *name, auto fn) {
+            cudaEvent_t a, b;
+            CK(cudaSetDevice(0));
+            CK(cudaEventCreate(&a));
+            CK(cudaEventCreate(&b));
+            for (int i = 0; i < 3; ++i) fn();
+            CK(cudaEventRecord(a));
+            for (int i = 0; i < 20; ++i) fn();
+            CK(cudaEventRecord(b));
+            CK(cudaEventSynchronize(b));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, a, b));
+            std::printf("{\"variant\": \"%s\", \"bytes_per_dir\": %zu, \"ms\": %.4f, \"gbs_per_dir\": %.1f}\n",
+                        name, bytes, ms / 20, bytes / (ms / 20 * 1e-3) / 1e9);
+            std::fflush(stdout);
+        };
+        one("oneway_push_u4", [&] { copy_kernel<4><<<g_sms * 2, 512>>>((const uint4 *)p.buf[0][0], (uint4 *)p.buf[1][2], n16); });
+        one("oneway_pull_u4", [&] { copy_kernel<4><<<g_sms * 2, 512>>>((const uint4 *)p.buf[1][0], (uint4 *)p.buf[0][2], n16); });
+        one("oneway_memcpy_peer", [&] { CK(cudaMemcpyPeerAsync(p.buf[1][2], 1, p.buf[0][0], 0, bytes, 0)); });
+    }
     // pull-reduce-push (the current fused kernel's traffic at N=2 on half the bytes each way)
     for (int grid_mult : {1, 2, 4}) {
         char name[64];

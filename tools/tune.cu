@@ -5,7 +5,10 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
 //        -o tools/tune tools/tune.cu
-//   ./tools/tune <world> <L> <f32|bf16> <sgd|mean> [iters]
+//   ./tools/tune <world> <L> <f32|bf16> <sgd|mean> [iters] [lib]
+// "lib": only the library's launch shape.  Every line carries a phase breakdown from
+// %globaltimer stamps (kernels built with GDRAA_TRACE).
+#define GDRAA_TRACE 1
 #include "../paper_1802_02326_b200/csrc/gdraa_kernels.cu"
 
 #include <cstdio>
@@ -38,6 +41,8 @@ static int DT, MODE_;
 static int ITERS = 50;
 static std::vector<Bufs> B;
 static ErrBlock *err_d;
+static std::vector<uint64_t *> TR;   // per-device trace ring (64 calls x 8 vr x 8 stamps)
+static bool LIB_ONLY = false;
 
 template <typename TG, int WORLD, int MODE, int U, int THREADS, int MINB>
 void run_shape(int grid_div) {
@@ -52,7 +57,7 @@ void run_shape(int grid_div) {
         (void)off; (void)len;
     }
     const uint64_t nvec = (blk + 3) / 4;
-    uint64_t want = (nvec + THREADS - 1) / THREADS;
+    uint64_t want = (nvec + THREADS * U - 1) / (THREADS * U);
     int gx = (int)std::min<uint64_t>(want, (uint64_t)sms * per / grid_div);
     if (gx < 1) gx = 1;
     std::vector<cudaStream_t> st(WORLD);
@@ -81,6 +86,7 @@ void run_shape(int grid_div) {
             }
             p.v[0] = B[d].v[set];
             p.err = err_d;
+            p.trace = TR[d];
             CK(cudaSetDevice(d));
             fn<<<dim3(gx, 1), THREADS, 0, st[d]>>>(p);
             CK(cudaGetLastError());
@@ -103,15 +109,37 @@ void run_shape(int grid_div) {
         std::fprintf(stderr, "timeout reported\n");
         std::exit(2);
     }
+    // phase breakdown from the %globaltimer stamps of the last calls (same-device deltas)
+    double acc[5] = {0, 0, 0, 0, 0};
+    int cnt = 0;
+    for (int d = 0; d < WORLD; ++d) {
+        std::vector<uint64_t> h(64 * kMaxWorld * 8);
+        CK(cudaSetDevice(d));
+        CK(cudaMemcpy(h.data(), TR[d], h.size() * 8, cudaMemcpyDeviceToHost));
+        for (int e = 0; e < 64; ++e) {
+            const uint64_t *a = &h[(e * kMaxWorld) * 8];
+            const uint64_t *b = &h[(((e + 1) % 64) * kMaxWorld) * 8];
+            if (!a[0] || !a[4] || !b[0] || b[0] < a[4] || b[0] - a[4] > 1000000) continue;
+            acc[0] += a[1] - a[0];
+            acc[1] += a[2] - a[1];
+            acc[2] += a[3] - a[2];
+            acc[3] += a[4] - a[3];
+            acc[4] += b[0] - a[4];
+            ++cnt;
+        }
+    }
     const double t = worst / ITERS * 1e-3;
     const int sg = sizeof(TG);
     double bytes = WORLD == 1 ? (MODE == kSgd ? (sg + 16.0) * L : 2.0 * sg * L)
                               : (WORLD - 1.0) / WORLD * L * (sg + (MODE == kSgd ? 4 : sg));
     std::printf("{\"world\": %d, \"L\": %zu, \"dtype\": \"%s\", \"mode\": \"%s\", \"U\": %d, "
                 "\"threads\": %d, \"minb\": %d, \"per_sm\": %d, \"grid\": %d, \"us\": %.2f, "
-                "\"gbs_per_rank\": %.1f}\n",
+                "\"gbs_per_rank\": %.1f, \"phase_us\": {\"entry\": %.2f, \"data_cta0\": %.2f, "
+                "\"to_last_arrival\": %.2f, \"exit\": %.2f, \"gap_to_next\": %.2f}}\n",
                 WORLD, L, sg == 4 ? "f32" : "bf16", MODE == kSgd ? "sgd" : "mean", U, THREADS,
-                MINB, per, gx, t * 1e6, bytes / t / 1e9);
+                MINB, per, gx, t * 1e6, bytes / t / 1e9, cnt ? acc[0] / cnt / 1e3 : 0.0,
+                cnt ? acc[1] / cnt / 1e3 : 0.0, cnt ? acc[2] / cnt / 1e3 : 0.0,
+                cnt ? acc[3] / cnt / 1e3 : 0.0, cnt ? acc[4] / cnt / 1e3 : 0.0);
     std::fflush(stdout);
     for (int d = 0; d < WORLD; ++d) {
         CK(cudaSetDevice(d));
@@ -121,6 +149,11 @@ void run_shape(int grid_div) {
 
 template <typename TG, int WORLD, int MODE>
 void sweep() {
+    if (LIB_ONLY) {
+        using S = Shape<TG, WORLD, MODE>;
+        run_shape<TG, WORLD, MODE, S::U, S::THREADS, S::MINB>(1);
+        return;
+    }
     run_shape<TG, WORLD, MODE, 1, 512, 1>(1);
     run_shape<TG, WORLD, MODE, 2, 512, 1>(1);
     run_shape<TG, WORLD, MODE, 4, 512, 1>(1);
@@ -156,6 +189,7 @@ int main(int argc, char **argv) {
     DT = std::string(argv[3]) == "bf16" ? GDRAA_BF16 : GDRAA_F32;
     MODE_ = std::string(argv[4]) == "mean" ? kMean : kSgd;
     if (argc > 5) ITERS = std::atoi(argv[5]);
+    if (argc > 6) LIB_ONLY = std::string(argv[6]) == "lib";
     CK(cudaGetDeviceCount(&NDEV));
     if (NDEV < W) {
         std::fprintf(stderr, "need %d GPUs, have %d\n", W, NDEV);
@@ -176,6 +210,10 @@ int main(int argc, char **argv) {
             CK(cudaMemset(B[d].v[s], 0, L * 4));
         }
         CK(cudaMalloc(&B[d].pad, sizeof(Pad)));
+        uint64_t *tr;
+        CK(cudaMalloc(&tr, 64 * kMaxWorld * 8 * 8));
+        CK(cudaMemset(tr, 0, 64 * kMaxWorld * 8 * 8));
+        TR.push_back(tr);
         CK(cudaMemset(B[d].pad, 0, sizeof(Pad)));
     }
     void *eh;
