@@ -35,7 +35,11 @@ CONFIGS = {
     "r50": (synth.L_R50, "f32", "config 2: ResNet-50 fp32 gradient buffer (25,557,032)"),
     "r101": (synth.L_R101, "f32", "config 3: ResNet-101 fp32 gradient buffer (44,549,160)"),
     "r50bf16": (synth.L_R50, "bf16", "config 4: ResNet-50 bf16 gradients, fp32 master w/v"),
+    "r50bf16mp": (synth.L_R50, "bf16", "config 4 + NEXT-1: bf16 gradients, fp32 master "
+                  "sharded like v, bf16 model copy all-gathered, weight decay 0.001"),
 }
+MP_CONFIGS = {"r50bf16mp"}
+PAPER_WD = 0.001               # P:246 "weight decay is 0.001"
 NVLINK_NOMINAL_GBS = 900.0     # NVLink 5, per direction per GPU
 NVLINK_MEASURED_GBS = 770.0    # B200_PROFILING.md: measured peer copy per direction
 
@@ -48,14 +52,16 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
-def algorithmic_bytes(L, N, s_g, shard_lens):
-    """Per-rank algorithmic bytes of one step.
-    N = 1: HBM bytes of the local fused SGD, (s_g + 16) * L (read g, w, v; write w, v).
-    N >= 2: NVLink bus bytes per rank per direction, B_nv = (N-1)/N * L * (s_g + 4)
-    (reduce ingress of g + broadcast ingress of w; NCCL busBW convention)."""
+def algorithmic_bytes(L, N, s_g, s_w=4):
+    """Per-rank algorithmic bytes of one step (DESIGN.md §6 "Roofline").
+    N = 1: HBM bytes of the local fused SGD, (s_g + 16) * L (read g, w, v; write w, v),
+    plus s_w * L for the separate model copy of the mixed-precision variant (s_w = 2).
+    N >= 2: NVLink bus bytes per rank per direction, B_nv = (N-1)/N * L * (s_g + s_w)
+    (reduce ingress of g + broadcast ingress of w' or its bf16 copy; NCCL busBW
+    convention)."""
     if N == 1:
-        return (s_g + 16) * L
-    return (N - 1) / N * L * (s_g + 4)
+        return (s_g + 16 + (s_w if s_w != 4 else 0)) * L
+    return (N - 1) / N * L * (s_g + s_w)
 
 
 # ---------------------------------------------------------------------------------------
@@ -129,21 +135,26 @@ class OracleSample:
     workload: the first n elements of every one of the N rank buffers (all N ranks are
     simulated in one process, as the oracle defines the method)."""
 
-    def __init__(self, L, N, g_dt, n=1 << 20):
+    def __init__(self, L, N, g_dt, mp=False, n=1 << 20):
         import oracle
-        self.oracle, self.L, self.N, self.n = oracle, L, N, min(L, n)
+        self.oracle, self.L, self.N, self.n, self.mp = oracle, L, N, min(L, n), mp
         self.gs = [synth.grad_like(0, p, self.n) for p in range(N)]
         if g_dt == "bf16":
             self.gs = [synth.to_bf16_bits_trunc(g) for g in self.gs]
         self.w, self.v = synth.w_like(0, self.n), np.zeros(self.n, np.float32)
         s_g = 2 if g_dt == "bf16" else 4
         # the metric's bytes for this sample, summed over ranks as `value` is
-        self.bytes = algorithmic_bytes(self.n, N, s_g, None) * N
+        self.bytes = algorithmic_bytes(self.n, N, s_g, 2 if mp else 4) * N
 
     def step(self):
         t0 = time.perf_counter()
-        self.w, self.v = self.oracle.sgd_step(self.gs, self.w, self.v, synth.PAPER_LR,
-                                              synth.PAPER_MOM)
+        if self.mp:
+            self.w, self.v, _ = self.oracle.sgd_step_wd(
+                self.gs, self.w, self.v, synth.PAPER_LR, synth.PAPER_MOM, PAPER_WD,
+                model_dtype=self.oracle.BF16)
+        else:
+            self.w, self.v = self.oracle.sgd_step(self.gs, self.w, self.v, synth.PAPER_LR,
+                                                  synth.PAPER_MOM)
         return time.perf_counter() - t0
 
     def describe(self, reps):
@@ -151,9 +162,9 @@ class OracleSample:
                 f"the {self.N} rank buffers (L={self.L}); single thread")
 
 
-def oracle_baseline(L, N, g_dt, budget_s):
+def oracle_baseline(L, N, g_dt, budget_s, mp=False):
     """(bytes/s, sample description, s/step) of the oracle over ~budget_s seconds."""
-    s = OracleSample(L, N, g_dt)
+    s = OracleSample(L, N, g_dt, mp)
     s.step()
     reps, total = 0, 0.0
     while total < budget_s:
@@ -170,7 +181,7 @@ def run_reference(args):
         return 0
     L, g_dt, desc = CONFIGS[args.config]
     N = args.gpus
-    s = OracleSample(L, N, g_dt)
+    s = OracleSample(L, N, g_dt, args.config in MP_CONFIGS)
     for _ in range(args.warmup):
         s.step()
     dts = [s.step() for _ in range(args.steps)]
@@ -192,8 +203,11 @@ def run_reference(args):
 
 
 def config_dict(args, L, g_dt, desc, N):
+    mp = args.config in MP_CONFIGS
     return {"workload": args.config, "description": desc, "L": L, "g_dtype": g_dt,
-            "w_dtype": "f32", "v_dtype": "f32", "lr": synth.PAPER_LR, "mom": synth.PAPER_MOM,
+            "w_dtype": "f32 master sharded + bf16 model copy" if mp else "f32",
+            "v_dtype": "f32", "lr": synth.PAPER_LR, "mom": synth.PAPER_MOM,
+            "wd": PAPER_WD if mp else 0.0,
             "parallelism": f"dp{N}", "buffer_sets": args.sets,
             "l2": f"inputs larger than L2: {args.sets} rotating (g, w, v) sets per rank"}
 
@@ -241,27 +255,47 @@ def main():
     gdraa.gdraa_init(world, rank)
 
     L, g_dt, desc = CONFIGS[args.config]
+    mp = args.config in MP_CONFIGS
     N = world
     s_g = 2 if g_dt == "bf16" else 4
+    s_w = 2 if mp else 4
     tdt = torch.bfloat16 if g_dt == "bf16" else torch.float32
     off, ln = gdraa.gdraa_shard(N, rank, L)
+    lr, mom = synth.PAPER_LR, synth.PAPER_MOM
+    wd = PAPER_WD if mp else 0.0
+    stream = torch.cuda.current_stream()
+
+    class StepSet:
+        """One (g, w, v) buffer set and the public call that steps it."""
+
+        def __init__(self, s):
+            g_h = synth.grad_like(100 + s, rank, L)
+            if g_dt == "bf16":
+                g_h = synth.to_bf16_bits_trunc(g_h).view(np.int16)
+            self.g = torch.from_numpy(g_h).to(dev)
+            self.g = self.g.view(tdt) if g_dt == "bf16" else self.g
+            self.w = torch.from_numpy(synth.w_like(100 + s, L)).to(dev)   # fp32 (master)
+            self.v = torch.zeros(L, dtype=torch.float32, device=dev)
+            if mp:   # NEXT-1: replicated bf16 model copy, fp32 master sharded like v
+                self.model = torch.zeros(L, dtype=torch.bfloat16, device=dev)
+                gdraa.gdraa_register(self.model)
+            else:
+                gdraa.gdraa_register(self.w)
+            gdraa.gdraa_register(self.g)
+
+        def step(self):
+            if mp:
+                gdraa.gdraa_sgd_step_mp(self.w, self.model, self.g, self.v, lr, mom, wd, stream)
+            else:
+                gdraa.gdraa_sgd_step(self.w, self.g, self.v, lr, mom, stream)
+
+        def result_shard(self):
+            """This rank's share of the step's result (read back by the e2e leg)."""
+            return (self.model if mp else self.w)[off:off + ln]
 
     # synthetic inputs (host), then resident in HBM; S rotating sets so that no step
     # finds its inputs in the 126 MB L2.
-    sets = []
-    for s in range(args.sets):
-        g_h = synth.grad_like(100 + s, rank, L)
-        if g_dt == "bf16":
-            g_h = synth.to_bf16_bits_trunc(g_h).view(np.int16)
-        g = torch.from_numpy(g_h).to(dev)
-        g = g.view(tdt) if g_dt == "bf16" else g
-        w = torch.from_numpy(synth.w_like(100 + s, L)).to(dev)
-        v = torch.zeros(L, dtype=torch.float32, device=dev)
-        gdraa.gdraa_register(w)
-        gdraa.gdraa_register(g)
-        sets.append((w, g, v))
-    lr, mom = synth.PAPER_LR, synth.PAPER_MOM
-    stream = torch.cuda.current_stream()
+    sets = [StepSet(s) for s in range(args.sets)]
 
     def barrier():
         if world > 1:
@@ -269,8 +303,7 @@ def main():
         torch.cuda.synchronize()
 
     for k in range(args.warmup):
-        w, g, v = sets[k % len(sets)]
-        gdraa.gdraa_sgd_step(w, g, v, lr, mom, stream)
+        sets[k % len(sets)].step()
     barrier()
 
     st0 = gdraa.gdraa_get_stats()
@@ -281,8 +314,7 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for k in range(args.steps):
-        w, g, v = sets[k % len(sets)]
-        gdraa.gdraa_sgd_step(w, g, v, lr, mom, stream)
+        sets[k % len(sets)].step()
     ev1.record(stream)
     torch.cuda.synchronize()
     if clocks:
@@ -296,22 +328,23 @@ def main():
     st1 = gdraa.gdraa_get_stats()
     launches = st1["launches"] - st0["launches"]
     ms_step = ms / args.steps
-    per_rank = algorithmic_bytes(L, N, s_g, None)
+    per_rank = algorithmic_bytes(L, N, s_g, s_w)
     value = per_rank * N / (ms_step * 1e-3) / 1e9           # whole job
     achieved = per_rank / (ms_step * 1e-3) / 1e9            # per rank = per launch
 
     # ---- e2e: host buffers through the public API, copies inside the timed region ----
+    st = sets[0]
     g_host = torch.empty(L, dtype=tdt, pin_memory=True)
-    g_host.copy_(sets[0][1].cpu())
-    w_out = torch.empty(ln, dtype=torch.float32, pin_memory=True)
-    w, g, v = sets[0]
+    g_host.copy_(st.g.cpu())
+    out_dev = st.result_shard()
+    out_host = torch.empty(ln, dtype=out_dev.dtype, pin_memory=True)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for k in range(args.e2e_steps):
-        g.copy_(g_host, non_blocking=True)
-        gdraa.gdraa_sgd_step(w, g, v, lr, mom, stream)
-        w_out.copy_(w[off:off + ln], non_blocking=True)
+        st.g.copy_(g_host, non_blocking=True)
+        st.step()
+        out_host.copy_(out_dev, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
     ems = e0.elapsed_time(e1)
@@ -324,7 +357,7 @@ def main():
     # ---- NCCL all_reduce(AVG) of the same gradient buffer (reference point) ----
     nccl = None
     if world > 1 and not args.no_nccl:
-        buf = sets[0][1].clone()
+        buf = sets[0].g.clone()
         for _ in range(5):
             dist.all_reduce(buf, op=dist.ReduceOp.AVG)
         barrier()
@@ -347,7 +380,7 @@ def main():
         if N == 1:
             roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                     "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src,
-                    "bytes_per_launch": per_rank, "bytes_per_element": s_g + 16}
+                    "bytes_per_launch": per_rank, "bytes_per_element": per_rank / L}
         else:
             roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_MEASURED_GBS,
                     "unit": "GB/s", "frac": achieved / NVLINK_MEASURED_GBS,
@@ -358,7 +391,7 @@ def main():
         roof["kernel_ms"] = ms_step
         cpu = None
         if N == 1 and not args.no_cpu_baseline:
-            cv, sample, _ = oracle_baseline(L, N, g_dt, 10.0)
+            cv, sample, _ = oracle_baseline(L, N, g_dt, 10.0, mp)
             cpu = {"value": cv / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
                    "sample": sample}
         line = {
@@ -368,14 +401,15 @@ def main():
             "dtype": "f32", "data": "synthetic",
             "config": config_dict(args, L, g_dt, desc, N),
             "value_definition": ("sum over ranks of per-rank algorithmic bytes / step time; "
-                                 + ("N=1: HBM bytes (s_g+16)*L" if N == 1 else
-                                    "N>=2: NVLink bus bytes (N-1)/N*L*(s_g+4) per rank")),
+                                 + (f"N=1: HBM bytes {per_rank / L:g}*L" if N == 1 else
+                                    f"N>=2: NVLink bus bytes (N-1)/N*L*({s_g}+{s_w}) per rank")),
             "bus_gbs_per_rank": achieved if N > 1 else 0.0,
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "GB/s", "steps": args.e2e_steps,
-                    "h2d_bytes_per_step": L * s_g * N, "d2h_bytes_per_step": L * 4,
+                    "h2d_bytes_per_step": L * s_g * N, "d2h_bytes_per_step": L * s_w,
                     "note": "all ranks: H2D of each rank's gradient from pinned host memory, "
-                            "gdraa_sgd_step, D2H of each rank's updated w shard"},
+                            "the step through the public API, D2H of each rank's shard of "
+                            "the updated weights"},
             "gpu_launches": launches, "clocks": clocks.summary() if clocks else None,
             "nccl_reference": nccl,
         }

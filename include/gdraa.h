@@ -127,6 +127,36 @@ int gdraa_allreduce_mean(void *buf, gdraa_stream_t s);
 int gdraa_sgd_step(float *w, const void *g, float *v, float lr, float mom, gdraa_stream_t s);
 
 /*
+ * gdraa_sgd_step_ex -- gdraa_sgd_step with weight decay wd ("weight decay is
+ * 0.001"; SGD form S:412 v <- mu*v + (g + lambda*w)).  Per element, before the
+ * momentum step: m = fl(m + fl(wd*w)).  wd == 0 forms no decay term, i.e. it is exactly
+ * gdraa_sgd_step.  Arguments and errors as gdraa_sgd_step; wd must be finite.
+ */
+int gdraa_sgd_step_ex(float *w, const void *g, float *v, float lr, float mom, float wd,
+                      gdraa_stream_t s);
+
+/*
+ * gdraa_sgd_step_mp -- mixed-precision variant: the fp32 master
+ * weights are sharded like the momentum, and the broadcast carries a bf16 model
+ * copy, cutting the all-gather bytes per element from 4 to 2.
+ *   w_master: f32 device buffer, n elements, rank-local (not registered); only the owner
+ *             shard [off_r, off_r + len_r) is read and written.
+ *   w_model:  registered GDRAA_BF16 buffer, n elements; after the call every rank holds
+ *             bf16 RNE(w') of every shard (w' = the updated fp32 master values).
+ *   g, v, lr, mom, wd: as gdraa_sgd_step_ex (g's dtype is f32 or bf16).
+ * Errors: EINVAL, ENOTREG, ESTATE, ETIMEOUT (sticky), ECUDA.
+ */
+int gdraa_sgd_step_mp(float *w_master, void *w_model, const void *g, float *v, float lr,
+                      float mom, float wd, gdraa_stream_t s);
+
+/*
+ * gdraa_poly_lr -- the paper's "poly" learning-rate policy with "gamma is 1" read as
+ * the power: lr0 * (1 - iter/max_iter)^power, in double, rounded
+ * once to float; 0 for iter >= max_iter; -1 if max_iter == 0.  Pure host function.
+ */
+float gdraa_poly_lr(float lr0, uint64_t iter, uint64_t max_iter, float power);
+
+/*
  * gdraa_shard -- the owner-shard partition ("Divide D(i) by N"; AMB-8):
  *   c = ceil(n/world); len = roundup(c, GDRAA_SHARD_QUANTUM);
  *   off_r = min(rank*len, n); len_r = min(len, n - off_r).
@@ -182,6 +212,12 @@ int gdraa_vr_allreduce_mean(int world, void *const *bufs, size_t n, int dtype,
                             gdraa_stream_t s);
 int gdraa_vr_sgd_step(int world, float *const *w, const void *const *g, float *const *v,
                       size_t n, int dtype, float lr, float mom, gdraa_stream_t s);
+int gdraa_vr_sgd_step_ex(int world, float *const *w, const void *const *g, float *const *v,
+                         size_t n, int dtype, float lr, float mom, float wd, gdraa_stream_t s);
+/* w_master: HOST array of per-rank f32 master buffers; w_model: per-rank bf16 buffers. */
+int gdraa_vr_sgd_step_mp(int world, float *const *w_master, void *const *w_model,
+                         const void *const *g, float *const *v, size_t n, int dtype, float lr,
+                         float mom, float wd, gdraa_stream_t s);
 
 #ifdef __cplusplus
 }

@@ -10,5 +10,5 @@ is "parity unpinned".
 """
 from .oracle import (  # noqa: F401
     F32, BF16, partition, bf16_to_f32, f32_to_bf16_rne, allreduce_mean, sgd_step, counters,
-    lib_path,
+    lib_path, sgd_step_wd, poly_lr,
 )

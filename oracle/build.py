@@ -20,7 +20,7 @@ def build(force: bool = False) -> str:
             and os.path.getmtime(LIB) >= max(os.path.getmtime(SRC),
                                              os.path.getmtime(os.path.join(HERE, "gdraa_oracle.h")))):
         return LIB
-    cmd = ["gcc", *CFLAGS, SRC, "-o", LIB + ".tmp"]
+    cmd = ["gcc", *CFLAGS, SRC, "-o", LIB + ".tmp", "-lm"]
     subprocess.run(cmd, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -8,6 +8,7 @@
  */
 #include "gdraa_oracle.h"
 
+#include <math.h>
 #include <string.h>
 
 /* P:185 "MiMatrix is designed for maximum 32 workers". */
@@ -98,6 +99,44 @@ int oracle_sgd_step(int N, uint64_t L, int dtype, const void *const *g, float *w
         w[i] = wn;
     }
     return 0;
+}
+
+int oracle_sgd_step_wd(int N, uint64_t L, int dtype, const void *const *g, float *w, float *v,
+                       float lr, float mom, float wd, void *model, int model_dtype)
+{
+    if (N < 1 || N > ORACLE_MAX_N || (dtype != ORACLE_F32 && dtype != ORACLE_BF16)) return -1;
+    if (L == 0) return -1;
+    if (model != 0 && model_dtype != ORACLE_F32 && model_dtype != ORACLE_BF16) return -1;
+    for (uint64_t i = 0; i < L; i++) {
+        float m = average_elem(N, dtype, g, i);
+        /* v <- mu*v + (g + lambda*w); w <- w - lr*v, one rounding per operation */
+        float ge = m;
+        if (wd != 0.0f) {
+            float d = wd * w[i];
+            ge = m + d;
+        }
+        float t = mom * v[i];
+        float vn = t + ge;
+        float u = lr * vn;
+        float wn = w[i] - u;
+        v[i] = vn;
+        w[i] = wn;
+        if (model != 0) {
+            if (model_dtype == ORACLE_F32)
+                ((float *)model)[i] = wn;
+            else
+                ((uint16_t *)model)[i] = oracle_f32_to_bf16_rne(wn);
+        }
+    }
+    return 0;
+}
+
+float oracle_poly_lr(float lr0, uint64_t iter, uint64_t max_iter, float power)
+{
+    if (max_iter == 0) return -1.0f;
+    if (iter >= max_iter) return 0.0f;
+    double frac = 1.0 - (double)iter / (double)max_iter;
+    return (float)((double)lr0 * pow(frac, (double)power));
 }
 
 int oracle_counters(uint64_t L, int N, uint64_t Q, int r, int s_g, int s_w,

@@ -60,6 +60,22 @@ int oracle_allreduce_mean(int N, uint64_t L, int dtype, const void *const *in, v
 int oracle_sgd_step(int N, uint64_t L, int dtype, const void *const *g, float *w, float *v,
                     float lr, float mom);
 
+/* The update with weight decay ("weight decay is 0.001"; SGD form S:412
+ * v <- mu*v + (g + lambda*w)), AMB-5: for every element i, with m the aggregation,
+ *   d = fl(wd * w[i]); ge = fl(m + d); t = fl(mom * v[i]); v[i] = fl(t + ge);
+ *   u = fl(lr * v[i]); w[i] = fl(w[i] - u)
+ * and, when wd == 0, exactly oracle_sgd_step (no decay term is formed).
+ * model (optional, may be NULL): the broadcast model copy in model_dtype, i.e. w[i]
+ * itself (f32) or bf16 RNE(w[i]) -- NEXT-1's mixed-precision all-gather, where the fp32
+ * master w is sharded like v and only the model copy travels.  Returns 0 or -1. */
+int oracle_sgd_step_wd(int N, uint64_t L, int dtype, const void *const *g, float *w, float *v,
+                       float lr, float mom, float wd, void *model, int model_dtype);
+
+/* "poly" learning-rate policy with "gamma" read as the power:
+ *   lr = lr0 * (1 - iter/max_iter)^power, evaluated in double, rounded once to float.
+ * Returns lr0 * 0 = 0 for iter >= max_iter; -1.0f on max_iter == 0. */
+float oracle_poly_lr(float lr0, uint64_t iter, uint64_t max_iter, float power);
+
 /* Lemma 1 / Lemma 2 accounting for rank r (Eq. 1-2, Eq. 3-4). */
 typedef struct {
     uint64_t rs_sent;     /* reduce: blocks j != r of D(r) leave r: s_g * (L - len_r)   (Eq. 1) */

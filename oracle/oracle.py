@@ -39,6 +39,10 @@ def _load():
         lib.oracle_sgd_step.restype = i32
         lib.oracle_counters.argtypes = [u64, i32, u64, i32, i32, i32, vp]
         lib.oracle_counters.restype = i32
+        lib.oracle_sgd_step_wd.argtypes = [i32, u64, i32, pvp, vp, vp, f32, f32, f32, vp, i32]
+        lib.oracle_sgd_step_wd.restype = i32
+        lib.oracle_poly_lr.argtypes = [f32, u64, u64, f32]
+        lib.oracle_poly_lr.restype = f32
         _lib = lib
     return _lib
 
@@ -108,6 +112,32 @@ def sgd_step(grads, w, v, lr: float, mom: float):
     if rc != 0:
         raise ValueError("oracle_sgd_step: invalid arguments")
     return w, v
+
+
+def sgd_step_wd(grads, w, v, lr: float, mom: float, wd: float, model_dtype=None):
+    """Momentum SGD with weight decay.  Returns (w, v) or, with
+    model_dtype in {F32, BF16}, (w, v, model) where model is the broadcast copy."""
+    dtype = _dtype_of(grads)
+    grads, ptrs = _ptrs(grads)
+    w = np.array(w, dtype=np.float32, copy=True)
+    v = np.array(v, dtype=np.float32, copy=True)
+    if w.shape != grads[0].shape or v.shape != grads[0].shape:
+        raise ValueError("w, v must match the gradient length")
+    model = None
+    if model_dtype is not None:
+        model = np.empty(w.shape, np.float32 if model_dtype == F32 else np.uint16)
+    rc = _load().oracle_sgd_step_wd(len(grads), grads[0].shape[0], dtype, ptrs, w.ctypes.data,
+                                    v.ctypes.data, float(lr), float(mom), float(wd),
+                                    None if model is None else model.ctypes.data,
+                                    F32 if model_dtype is None else model_dtype)
+    if rc != 0:
+        raise ValueError("oracle_sgd_step_wd: invalid arguments")
+    return (w, v) if model is None else (w, v, model)
+
+
+def poly_lr(lr0: float, it: int, max_iter: int, power: float) -> float:
+    """lr0 * (1 - it/max_iter)^power (P:246 "poly", S:455)."""
+    return float(_load().oracle_poly_lr(lr0, it, max_iter, power))
 
 
 def counters(L: int, N: int, r: int, s_g: int, s_w: int, Q: int = 64) -> dict:

@@ -48,10 +48,12 @@ struct KParams {
     uint64_t n;          // elements
     uint64_t blk;        // shard length (Q-aligned ceil(n/world))
     float lr, mom;
+    float wd;            // weight decay (0: no decay term is formed)
     uint64_t timeout_ns;
     const void *src[kMaxWorld][kMaxWorld];   // [vr][p]: rank p's g (or buf) seen from vr
     void *dst[kMaxWorld][kMaxWorld];         // [vr][p]: rank p's w (or buf) seen from vr
     float *v[kMaxWorld];                     // [vr]: local momentum buffer
+    float *wm[kMaxWorld];                    // [vr]: local fp32 master weights (kSgdMp)
     Pad *pad[kMaxWorld][kMaxWorld];          // [vr][p]: rank p's pad seen from vr
     ErrBlock *err;                           // host-mapped (device alias)
     volatile uint64_t *done[kMaxWorld];      // host-mapped done flags (device alias) or null
@@ -60,7 +62,10 @@ struct KParams {
 #endif
 };
 
-enum Mode { kMean = 0, kSgd = 1 };
+// kMean: dst = mean (allreduce_mean).  kSgd: dst = w' (fp32, replicated w).
+// kSgdMp: fp32 master w sharded like v (p.wm), dst = bf16 RNE(w') model copy (NEXT-1).
+enum Mode { kMean = 0, kSgd = 1, kSgdMp = 2 };
+constexpr int kModes = 3;
 
 // Launch the fused kernel.  grid_x CTAs per (virtual) rank; vr_rows = gridDim.y.
 // cooperative: use cudaLaunchCooperativeKernel (required when vr_rows > 1).

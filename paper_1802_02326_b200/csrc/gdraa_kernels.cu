@@ -171,8 +171,10 @@ __device__ __forceinline__ float average(const float (&x)[WORLD]) {
     return __fdiv_rn(s, static_cast<float>(WORLD));
 }
 
-// Update: v = fl(fl(mom*v) + m); w = fl(w - fl(lr*v)).
-__device__ __forceinline__ void sgd(float m, float lr, float mom, float &w, float &v) {
+// Update: v = fl(fl(mom*v) + m); w = fl(w - fl(lr*v)).  With weight decay
+// (P:246): m is first replaced by fl(m + fl(wd*w)); wd == 0 forms no decay term.
+__device__ __forceinline__ void sgd(float m, float lr, float mom, float wd, float &w, float &v) {
+    if (wd != 0.0f) m = __fadd_rn(m, __fmul_rn(wd, w));
     const float t = __fmul_rn(mom, v);
     v = __fadd_rn(t, m);
     const float u = __fmul_rn(lr, v);
@@ -233,9 +235,12 @@ gdraa_kernel(const __grid_constant__ KParams p) {
     const uint64_t len = min(p.blk, p.n - off);
     const uint64_t nvec = len / E;
 
-    const float lr = p.lr, mom = p.mom;
+    constexpr bool kUpdate = MODE != kMean;
+    const float lr = p.lr, mom = p.mom, wd = p.wd;
     float *const vloc = p.v[vr];
-    const float *const wloc = static_cast<const float *>(p.dst[vr][rank]);
+    // the fp32 weights the update reads: the replicated w (kSgd) or the local master
+    // shard (kSgdMp, whose broadcast carries only a bf16 model copy)
+    float *const wloc = MODE == kSgdMp ? p.wm[vr] : static_cast<float *>(p.dst[vr][rank]);
     const Raw *src[WORLD];
 #pragma unroll
     for (int q = 0; q < WORLD; ++q)
@@ -252,7 +257,7 @@ gdraa_kernel(const __grid_constant__ KParams p) {
             const uint64_t k = k0 + u * THREADS;
 #pragma unroll
             for (int q = 0; q < WORLD; ++q) raw[u][q] = ld_stream(src[q] + k);
-            if (MODE == kSgd) {
+            if (kUpdate) {
                 wv[u] = ld_f4(wloc + off + k * E);
                 vv[u] = ld_f4(vloc + off + k * E);
             }
@@ -272,18 +277,31 @@ gdraa_kernel(const __grid_constant__ KParams p) {
                 for (int q = 0; q < WORLD; ++q) col[q] = x[q][e];
                 m[e] = average<WORLD>(col);
             }
-            if (MODE == kSgd) {
+            if (kUpdate) {
                 float4 w = wv[u], v = vv[u];
-                sgd(m[0], lr, mom, w.x, v.x);
-                sgd(m[1], lr, mom, w.y, v.y);
-                sgd(m[2], lr, mom, w.z, v.z);
-                sgd(m[3], lr, mom, w.w, v.w);
+                sgd(m[0], lr, mom, wd, w.x, v.x);
+                sgd(m[1], lr, mom, wd, w.y, v.y);
+                sgd(m[2], lr, mom, wd, w.z, v.z);
+                sgd(m[3], lr, mom, wd, w.w, v.w);
                 st_vec(reinterpret_cast<uint4 *>(vloc + e0), as_u4(v.x, v.y, v.z, v.w));
-                const uint4 o = as_u4(w.x, w.y, w.z, w.w);
+                if (MODE == kSgd) {
+                    const uint4 o = as_u4(w.x, w.y, w.z, w.w);
 #pragma unroll
-                for (int j = 1; j <= WORLD; ++j) {   // own copy last
-                    const int q = (rank + j) % WORLD;
-                    st_vec(reinterpret_cast<uint4 *>(static_cast<float *>(p.dst[vr][q]) + e0), o);
+                    for (int j = 1; j <= WORLD; ++j) {   // own copy last
+                        const int q = (rank + j) % WORLD;
+                        st_vec(reinterpret_cast<uint4 *>(static_cast<float *>(p.dst[vr][q]) + e0),
+                               o);
+                    }
+                } else {   // kSgdMp: master shard stays local, bf16 copy to every rank
+                    st_vec(reinterpret_cast<uint4 *>(wloc + e0), as_u4(w.x, w.y, w.z, w.w));
+                    const float wf[E] = {w.x, w.y, w.z, w.w};
+                    const uint2 o = Elem<__nv_bfloat16>::narrow(wf);
+#pragma unroll
+                    for (int j = 1; j <= WORLD; ++j) {
+                        const int q = (rank + j) % WORLD;
+                        st_vec(reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(p.dst[vr][q]) + e0),
+                               o);
+                    }
                 }
             } else {
                 const Raw o = EL::narrow(m);
@@ -332,12 +350,18 @@ gdraa_kernel(const __grid_constant__ KParams p) {
 #pragma unroll
             for (int q = 0; q < WORLD; ++q) col[q] = EL::load1(p.src[vr][q], e);
             const float m = average<WORLD>(col);
-            if (MODE == kSgd) {
+            if (kUpdate) {
                 float w = wloc[e], v = vloc[e];
-                sgd(m, lr, mom, w, v);
+                sgd(m, lr, mom, wd, w, v);
                 vloc[e] = v;
-                for (int j = 1; j <= WORLD; ++j)
-                    static_cast<float *>(p.dst[vr][(rank + j) % WORLD])[e] = w;
+                if (MODE == kSgd) {
+                    for (int j = 1; j <= WORLD; ++j)
+                        static_cast<float *>(p.dst[vr][(rank + j) % WORLD])[e] = w;
+                } else {
+                    wloc[e] = w;
+                    for (int j = 1; j <= WORLD; ++j)
+                        Elem<__nv_bfloat16>::store1(p.dst[vr][(rank + j) % WORLD], e, w);
+                }
             } else {
                 for (int j = 1; j <= WORLD; ++j) EL::store1(p.dst[vr][(rank + j) % WORLD], e, m);
             }
@@ -426,10 +450,18 @@ Launch pick_m(int world) {
     }
 }
 
+template <typename TG>
+Launch pick_t(int mode, int world) {
+    switch (mode) {
+        case kMean: return pick_m<TG, kMean>(world);
+        case kSgd: return pick_m<TG, kSgd>(world);
+        case kSgdMp: return pick_m<TG, kSgdMp>(world);
+        default: return {nullptr, 0, 0};
+    }
+}
+
 Launch pick(int dtype, int mode, int world) {
-    if (dtype == GDRAA_F32)
-        return mode == kSgd ? pick_m<float, kSgd>(world) : pick_m<float, kMean>(world);
-    return mode == kSgd ? pick_m<__nv_bfloat16, kSgd>(world) : pick_m<__nv_bfloat16, kMean>(world);
+    return dtype == GDRAA_F32 ? pick_t<float>(mode, world) : pick_t<__nv_bfloat16>(mode, world);
 }
 
 }  // namespace
@@ -440,8 +472,8 @@ int max_ctas(int dtype, int mode, int world) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
     // co-resident CTAs per device and kernel, queried once (it is on the launch path)
-    static int cache[64][2][2][kMaxWorld + 1];
-    int &c = cache[dev][dtype == GDRAA_F32 ? 0 : 1][mode == kSgd ? 1 : 0][world];
+    static int cache[64][2][kModes][kMaxWorld + 1];
+    int &c = cache[dev][dtype == GDRAA_F32 ? 0 : 1][mode][world];
     if (c == 0) {
         int sms = 0, per_sm = 0;
         if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)

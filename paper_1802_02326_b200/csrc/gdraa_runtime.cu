@@ -330,10 +330,11 @@ void fill_common(KParams &p, uint64_t n) {
     p.done[0] = g.done_d;
 }
 
-void account(uint64_t n, int dtype_g, bool sgd) {
+// Lemma 1/2 accounting of one call (s_w: bytes per broadcast element; 0 = same as g).
+void account(uint64_t n, int dtype_g, uint64_t s_w) {
     uint64_t blk, off, len;
     partition(n, g.world, g.rank, &blk, &off, &len);
-    const uint64_t sg = elem_size(dtype_g), sw = sgd ? 4 : sg, n1 = g.world - 1;
+    const uint64_t sg = elem_size(dtype_g), sw = s_w ? s_w : sg, n1 = g.world - 1;
     g.host.rs_bytes_in += sg * n1 * len;
     g.host.rs_bytes_out += sg * (n - len);
     g.host.ag_bytes_out += sw * n1 * len;
@@ -392,20 +393,41 @@ int vr_prepare(int world, VrDevice **out) {
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-int vr_run(int world, const void *const *src, void *const *dst, float *const *v, size_t n,
-           int dtype, float lr, float mom, int mode, cudaStream_t s) {
+// One virtual-rank call: src = g (or buf), dst = w / buf / bf16 model copy, v and wm
+// (master, kSgdMp only) rank-local.
+struct VrArgs {
+    int world;
+    const void *const *src;
+    void *const *dst;
+    float *const *v;
+    float *const *wm;
+    size_t n;
+    int dtype;
+    float lr, mom, wd;
+    int mode;
+};
+
+int vr_run(const VrArgs &a, cudaStream_t s) {
+    const int world = a.world, mode = a.mode;
+    const bool upd = mode != kMean;
     if (world < 1 || world > kMaxWorld) return fail(GDRAA_EINVAL, "world %d out of [1,%d]", world, kMaxWorld);
-    if (n == 0) return fail(GDRAA_EINVAL, "n must be >= 1");
-    if (dtype != GDRAA_F32 && dtype != GDRAA_BF16) return fail(GDRAA_EINVAL, "bad dtype %d", dtype);
-    if (src == nullptr || dst == nullptr || (mode == kSgd && v == nullptr))
+    if (a.n == 0) return fail(GDRAA_EINVAL, "n must be >= 1");
+    if (a.dtype != GDRAA_F32 && a.dtype != GDRAA_BF16) return fail(GDRAA_EINVAL, "bad dtype %d", a.dtype);
+    if (a.src == nullptr || a.dst == nullptr || (upd && a.v == nullptr) ||
+        (mode == kSgdMp && a.wm == nullptr))
         return fail(GDRAA_EINVAL, "null pointer array");
-    if (mode == kSgd && !(std::isfinite(lr) && std::isfinite(mom)))
-        return fail(GDRAA_EINVAL, "lr and mom must be finite");
+    if (upd && !(std::isfinite(a.lr) && std::isfinite(a.mom) && std::isfinite(a.wd)))
+        return fail(GDRAA_EINVAL, "lr, mom and wd must be finite");
     for (int q = 0; q < world; ++q) {
-        if (src[q] == nullptr || dst[q] == nullptr || !aligned16(src[q]) || !aligned16(dst[q]) ||
-            (mode == kSgd && (v[q] == nullptr || !aligned16(v[q]))))
+        if (a.src[q] == nullptr || a.dst[q] == nullptr || !aligned16(a.src[q]) ||
+            !aligned16(a.dst[q]) || (upd && (a.v[q] == nullptr || !aligned16(a.v[q]))) ||
+            (mode == kSgdMp && (a.wm[q] == nullptr || !aligned16(a.wm[q]))))
             return fail(GDRAA_EINVAL, "rank %d: null or non-16-byte-aligned buffer", q);
     }
+    const int dtype = a.dtype;
+    const size_t n = a.n;
+    const void *const *src = a.src;
+    void *const *dst = a.dst;
     VrDevice *d = nullptr;
     int rc = vr_prepare(world, &d);
     if (rc) return rc;
@@ -416,8 +438,9 @@ int vr_run(int world, const void *const *src, void *const *dst, float *const *v,
     p.n = n;
     uint64_t off, len;
     partition(n, world, 0, &p.blk, &off, &len);
-    p.lr = lr;
-    p.mom = mom;
+    p.lr = a.lr;
+    p.mom = a.mom;
+    p.wd = a.wd;
     p.timeout_ns = env_u64("GDRAA_TIMEOUT_MS", 30000) * 1000000ull;
     for (int r = 0; r < world; ++r) {
         for (int q = 0; q < world; ++q) {
@@ -425,7 +448,8 @@ int vr_run(int world, const void *const *src, void *const *dst, float *const *v,
             p.dst[r][q] = dst[q];
             p.pad[r][q] = d->pads[world] + q;
         }
-        p.v[r] = mode == kSgd ? v[r] : nullptr;
+        p.v[r] = upd ? a.v[r] : nullptr;
+        p.wm[r] = mode == kSgdMp ? a.wm[r] : nullptr;
     }
     p.err = d->err_d;
     int gx = 0;
@@ -599,38 +623,72 @@ int gdraa_allreduce_mean(void *buf, gdraa_stream_t s) {
     }
     rc = launch(p, r->dtype, kMean, reinterpret_cast<cudaStream_t>(s));
     if (rc) return rc;
-    account(r->n, r->dtype, false);
+    account(r->n, r->dtype, 0);
     return GDRAA_OK;
 }
 
-int gdraa_sgd_step(float *w, const void *gr, float *v, float lr, float mom, gdraa_stream_t s) {
+// Shared body of gdraa_sgd_step / _ex (mode kSgd: dst = replicated fp32 w) and
+// gdraa_sgd_step_mp (mode kSgdMp: dst = replicated bf16 model copy, wm = local master).
+static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, float lr,
+                      float mom, float wd, gdraa_stream_t s) {
     std::lock_guard<std::mutex> lk(g_mu);
     int rc = check_sticky();
     if (rc) return rc;
-    if (!(std::isfinite(lr) && std::isfinite(mom))) return fail(GDRAA_EINVAL, "lr and mom must be finite");
-    const Registration *rw = find_reg(w);
+    if (!(std::isfinite(lr) && std::isfinite(mom) && std::isfinite(wd)))
+        return fail(GDRAA_EINVAL, "lr, mom and wd must be finite");
+    const char *dname = mode == kSgd ? "w" : "w_model";
+    const Registration *rw = find_reg(dst);
     const Registration *rg = find_reg(gr);
-    if (rw == nullptr) return fail(GDRAA_ENOTREG, "w %p is not registered", static_cast<void *>(w));
+    if (rw == nullptr) return fail(GDRAA_ENOTREG, "%s %p is not registered", dname, dst);
     if (rg == nullptr) return fail(GDRAA_ENOTREG, "g %p is not registered", gr);
-    if (rw->dtype != GDRAA_F32) return fail(GDRAA_EINVAL, "w must be registered as GDRAA_F32");
-    if (rw->n != rg->n) return fail(GDRAA_EINVAL, "w (n=%zu) and g (n=%zu) differ in length", rw->n, rg->n);
-    if (rw == rg) return fail(GDRAA_EINVAL, "w and g must be distinct buffers");
+    const int want = mode == kSgd ? GDRAA_F32 : GDRAA_BF16;
+    if (rw->dtype != want)
+        return fail(GDRAA_EINVAL, "%s must be registered as %s", dname,
+                    want == GDRAA_F32 ? "GDRAA_F32" : "GDRAA_BF16");
+    if (rw->n != rg->n)
+        return fail(GDRAA_EINVAL, "%s (n=%zu) and g (n=%zu) differ in length", dname, rw->n, rg->n);
+    if (rw == rg) return fail(GDRAA_EINVAL, "%s and g must be distinct buffers", dname);
     if (v == nullptr || !aligned16(v)) return fail(GDRAA_EINVAL, "v is null or not 16-byte aligned");
+    if (mode == kSgdMp && (wm == nullptr || !aligned16(wm)))
+        return fail(GDRAA_EINVAL, "w_master is null or not 16-byte aligned");
     rc = wait_go();
     if (rc) return rc;
     KParams p;
     fill_common(p, rw->n);
     p.lr = lr;
     p.mom = mom;
+    p.wd = wd;
     for (int q = 0; q < g.world; ++q) {
         p.src[0][q] = rg->peer[q];
         p.dst[0][q] = rw->peer[q];
     }
     p.v[0] = v;
-    rc = launch(p, rg->dtype, kSgd, reinterpret_cast<cudaStream_t>(s));
+    p.wm[0] = mode == kSgdMp ? wm : nullptr;
+    rc = launch(p, rg->dtype, mode, reinterpret_cast<cudaStream_t>(s));
     if (rc) return rc;
-    account(rw->n, rg->dtype, true);
+    account(rw->n, rg->dtype, mode == kSgd ? 4 : 2);
     return GDRAA_OK;
+}
+
+int gdraa_sgd_step(float *w, const void *gr, float *v, float lr, float mom, gdraa_stream_t s) {
+    return sgd_common(kSgd, nullptr, w, gr, v, lr, mom, 0.0f, s);
+}
+
+int gdraa_sgd_step_ex(float *w, const void *gr, float *v, float lr, float mom, float wd,
+                      gdraa_stream_t s) {
+    return sgd_common(kSgd, nullptr, w, gr, v, lr, mom, wd, s);
+}
+
+int gdraa_sgd_step_mp(float *w_master, void *w_model, const void *gr, float *v, float lr,
+                      float mom, float wd, gdraa_stream_t s) {
+    return sgd_common(kSgdMp, w_master, w_model, gr, v, lr, mom, wd, s);
+}
+
+float gdraa_poly_lr(float lr0, uint64_t iter, uint64_t max_iter, float power) {
+    if (max_iter == 0) return -1.0f;
+    if (iter >= max_iter) return 0.0f;
+    const double frac = 1.0 - static_cast<double>(iter) / static_cast<double>(max_iter);
+    return static_cast<float>(static_cast<double>(lr0) * std::pow(frac, static_cast<double>(power)));
 }
 
 int gdraa_get_stats(gdraa_stats_t *out) {
@@ -682,15 +740,29 @@ int gdraa_finalize(void) {
 
 int gdraa_vr_allreduce_mean(int world, void *const *bufs, size_t n, int dtype, gdraa_stream_t s) {
     std::lock_guard<std::mutex> lk(g_mu);
-    return vr_run(world, reinterpret_cast<const void *const *>(bufs), bufs, nullptr, n, dtype, 0.f,
-                  0.f, kMean, reinterpret_cast<cudaStream_t>(s));
+    VrArgs a{world, reinterpret_cast<const void *const *>(bufs), bufs, nullptr, nullptr, n, dtype,
+             0.f, 0.f, 0.f, kMean};
+    return vr_run(a, reinterpret_cast<cudaStream_t>(s));
 }
 
 int gdraa_vr_sgd_step(int world, float *const *w, const void *const *g_, float *const *v, size_t n,
                       int dtype, float lr, float mom, gdraa_stream_t s) {
+    return gdraa_vr_sgd_step_ex(world, w, g_, v, n, dtype, lr, mom, 0.0f, s);
+}
+
+int gdraa_vr_sgd_step_ex(int world, float *const *w, const void *const *g_, float *const *v,
+                         size_t n, int dtype, float lr, float mom, float wd, gdraa_stream_t s) {
     std::lock_guard<std::mutex> lk(g_mu);
-    return vr_run(world, g_, reinterpret_cast<void *const *>(w), v, n, dtype, lr, mom, kSgd,
-                  reinterpret_cast<cudaStream_t>(s));
+    VrArgs a{world, g_, reinterpret_cast<void *const *>(w), v, nullptr, n, dtype, lr, mom, wd, kSgd};
+    return vr_run(a, reinterpret_cast<cudaStream_t>(s));
+}
+
+int gdraa_vr_sgd_step_mp(int world, float *const *w_master, void *const *w_model,
+                         const void *const *g_, float *const *v, size_t n, int dtype, float lr,
+                         float mom, float wd, gdraa_stream_t s) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    VrArgs a{world, g_, w_model, v, w_master, n, dtype, lr, mom, wd, kSgdMp};
+    return vr_run(a, reinterpret_cast<cudaStream_t>(s));
 }
 
 }  // extern "C"

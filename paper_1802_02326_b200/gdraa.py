@@ -19,7 +19,9 @@ GDRAA_MAX_WORLD = 8
 ERRORS = {0: "GDRAA_OK", -1: "GDRAA_EINVAL", -2: "GDRAA_ENOTREG", -3: "GDRAA_ESHAPE",
           -4: "GDRAA_ECUDA", -5: "GDRAA_ETIMEOUT", -6: "GDRAA_ESTATE", -7: "GDRAA_EJOBSERVER"}
 
-EXPORTED = ["gdraa_init", "gdraa_register", "gdraa_deregister","gdraa_allreduce_mean", "gdraa_sgd_step",
+EXPORTED = ["gdraa_sgd_step_ex", "gdraa_sgd_step_mp", "gdraa_poly_lr",
+            "gdraa_vr_sgd_step_ex", "gdraa_vr_sgd_step_mp",
+            "gdraa_init", "gdraa_register", "gdraa_deregister","gdraa_allreduce_mean", "gdraa_sgd_step",
             "gdraa_shard", "gdraa_get_stats", "gdraa_finalize", "gdraa_last_error",
             "gdraa_version", "gdraa_vr_allreduce_mean", "gdraa_vr_sgd_step"]
 
@@ -58,6 +60,13 @@ _sig = {
     "gdraa_vr_allreduce_mean": ([_i, ctypes.POINTER(_vp), _sz, _i, _vp], _i),
     "gdraa_vr_sgd_step": ([_i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                            _sz, _i, _f, _f, _vp], _i),
+    "gdraa_sgd_step_ex": ([_vp, _vp, _vp, _f, _f, _f, _vp], _i),
+    "gdraa_sgd_step_mp": ([_vp, _vp, _vp, _vp, _f, _f, _f, _vp], _i),
+    "gdraa_poly_lr": ([_f, ctypes.c_uint64, ctypes.c_uint64, _f], _f),
+    "gdraa_vr_sgd_step_ex": ([_i, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                              ctypes.POINTER(_vp), _sz, _i, _f, _f, _f, _vp], _i),
+    "gdraa_vr_sgd_step_mp": ([_i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                              ctypes.POINTER(_vp), _sz, _i, _f, _f, _f, _vp], _i),
 }
 for _name, (_args, _res) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -130,6 +139,21 @@ def gdraa_sgd_step(w, g, v, lr: float, mom: float, stream=None):
            "gdraa_sgd_step")
 
 
+def gdraa_sgd_step_ex(w, g, v, lr: float, mom: float, wd: float, stream=None):
+    _check(_lib.gdraa_sgd_step_ex(_ptr(w), _ptr(g), _ptr(v), lr, mom, wd, _stream(stream)),
+           "gdraa_sgd_step_ex")
+
+
+def gdraa_sgd_step_mp(w_master, w_model, g, v, lr: float, mom: float, wd: float = 0.0,
+                      stream=None):
+    _check(_lib.gdraa_sgd_step_mp(_ptr(w_master), _ptr(w_model), _ptr(g), _ptr(v), lr, mom, wd,
+                                  _stream(stream)), "gdraa_sgd_step_mp")
+
+
+def gdraa_poly_lr(lr0: float, it: int, max_iter: int, power: float = 1.0) -> float:
+    return float(_lib.gdraa_poly_lr(lr0, it, max_iter, power))
+
+
 def gdraa_shard(world: int, rank: int, n: int):
     off, ln = ctypes.c_size_t(), ctypes.c_size_t()
     _check(_lib.gdraa_shard(world, rank, n, ctypes.byref(off), ctypes.byref(ln)), "gdraa_shard")
@@ -162,3 +186,18 @@ def gdraa_vr_sgd_step(w, g, v, lr: float, mom: float, stream=None):
     _check(_lib.gdraa_vr_sgd_step(len(g), _ptr_array(w), _ptr_array(g), _ptr_array(v), n,
                                   dtype_code(g[0]), lr, mom, _stream(stream)),
            "gdraa_vr_sgd_step")
+
+
+def gdraa_vr_sgd_step_ex(w, g, v, lr: float, mom: float, wd: float, stream=None):
+    n = g[0].numel()
+    _check(_lib.gdraa_vr_sgd_step_ex(len(g), _ptr_array(w), _ptr_array(g), _ptr_array(v), n,
+                                     dtype_code(g[0]), lr, mom, wd, _stream(stream)),
+           "gdraa_vr_sgd_step_ex")
+
+
+def gdraa_vr_sgd_step_mp(w_master, w_model, g, v, lr: float, mom: float, wd: float = 0.0,
+                         stream=None):
+    n = g[0].numel()
+    _check(_lib.gdraa_vr_sgd_step_mp(len(g), _ptr_array(w_master), _ptr_array(w_model),
+                                     _ptr_array(g), _ptr_array(v), n, dtype_code(g[0]), lr, mom,
+                                     wd, _stream(stream)), "gdraa_vr_sgd_step_mp")

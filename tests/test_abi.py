@@ -85,3 +85,13 @@ def test_calls_before_init_fail_cleanly():
             fn(*args)
         assert e.value.name == "GDRAA_ESTATE", fn
     assert "gdraa_init" in gdraa.gdraa_last_error()
+
+
+def test_poly_lr_matches_oracle(golden):
+    ex = golden["poly_lr"][0]
+    assert gdraa.gdraa_poly_lr(ex["lr0"], ex["iter"], ex["max_iter"], ex["power"]) == \
+        oracle.poly_lr(ex["lr0"], ex["iter"], ex["max_iter"], ex["power"])
+    for it in range(0, 5000, 37):
+        for power in (0.5, 1.0, 2.0):
+            assert gdraa.gdraa_poly_lr(0.1, it, 4999, power) == oracle.poly_lr(0.1, it, 4999, power)
+    assert gdraa.gdraa_poly_lr(0.1, 1, 0, 1.0) == -1.0

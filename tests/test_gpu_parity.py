@@ -257,3 +257,57 @@ def test_graph_capture_replays():
     torch.cuda.synchronize()
     for r in range(N):
         compare(from_dev(w_d[r]), w_ref, "f32", what=f"graph w rank {r}")
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT-1: weight decay and the mixed-precision (bf16 model copy) all-gather.
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("family", ["int", "like"])
+def test_vr_sgd_step_ex_weight_decay(N, dt, family):
+    bf16 = dt == "bf16"
+    wd = 2.0**-4 if family == "int" else 0.001          # weight decay 0.001
+    for L in (1, 257, 70_001, 1 << 20):
+        gs = make_grads(family, 400 + N, N, L, bf16)
+        w0, v0, lr, mom = make_wv(family, 400 + N, L)
+        w_exp, v_exp = oracle.sgd_step_wd(gs, w0, v0, lr, mom, wd)
+        g_d = [to_dev(g, bf16) for g in gs]
+        w_d = [to_dev(w0) for _ in range(N)]
+        v_d = [to_dev(v0) for _ in range(N)]
+        gdraa.gdraa_vr_sgd_step_ex(w_d, g_d, v_d, lr, mom, wd)
+        torch.cuda.synchronize()
+        for r in range(N):
+            compare(from_dev(w_d[r]), w_exp, "f32", what=f"w N={N} L={L} rank {r}")
+            off, ln = gdraa.gdraa_shard(N, r, L)
+            compare(from_dev(v_d[r])[off:off + ln], v_exp[off:off + ln], "f32", what=f"v r{r}")
+
+
+@pytest.mark.parametrize("N", [1, 2, 4, 5, 8])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_vr_sgd_step_mp(N, dt):
+    """fp32 master sharded like v; every rank receives bf16 RNE(w') of every shard."""
+    bf16 = dt == "bf16"
+    for L in (1, 5, 1000, 70_001, 1 << 20):
+        gs = make_grads("like", 500 + N, N, L, bf16)
+        w0, v0 = synth.w_like(500 + N, L), synth.w_like(600 + N, L)
+        w_exp, v_exp, model_exp = oracle.sgd_step_wd(gs, w0, v0, synth.PAPER_LR,
+                                                     synth.PAPER_MOM, 0.001,
+                                                     model_dtype=oracle.BF16)
+        g_d = [to_dev(g, bf16) for g in gs]
+        wm_d = [to_dev(w0) for _ in range(N)]
+        v_d = [to_dev(v0) for _ in range(N)]
+        model_d = [torch.zeros(L, dtype=torch.bfloat16, device=DEV) for _ in range(N)]
+        gdraa.gdraa_vr_sgd_step_mp(wm_d, model_d, g_d, v_d, synth.PAPER_LR, synth.PAPER_MOM,
+                                   0.001)
+        torch.cuda.synchronize()
+        for r in range(N):
+            compare(from_dev(model_d[r]), model_exp, "bf16", what=f"model N={N} L={L} r{r}")
+            off, ln = gdraa.gdraa_shard(N, r, L)
+            wm = from_dev(wm_d[r])
+            compare(wm[off:off + ln], w_exp[off:off + ln], "f32", what=f"master r{r}")
+            compare(from_dev(v_d[r])[off:off + ln], v_exp[off:off + ln], "f32", what=f"v r{r}")
+            keep = np.ones(L, bool)
+            keep[off:off + ln] = False
+            assert np.array_equal(wm[keep].view(np.uint32), w0[keep].view(np.uint32))

@@ -65,6 +65,28 @@ def _worker(rank, world, sock, L_list, out_dir):
                     compare(from_dev(v)[off:off + ln], v0[off:off + ln], "f32",
                             what=f"v it{it} L={L} {dt} {family} r{rank}")
                 assert np.array_equal(from_dev(g), gs[rank])     # g read-only (AMB-18)
+                # NEXT-1: weight decay and the mixed-precision all-gather (bf16 model copy)
+                w0, v0 = synth.w_like(6, L), synth.w_like(7, L)
+                we, ve, me = oracle.sgd_step_wd(gs, w0, v0, lr, mom, 0.001,
+                                                model_dtype=oracle.BF16)
+                wm, vm = to_dev(w0, dev=dev), to_dev(v0, dev=dev)
+                model = torch.zeros(L, dtype=torch.bfloat16, device=dev)
+                gdraa.gdraa_register(model)
+                gdraa.gdraa_sgd_step_mp(wm, model, g, vm, lr, mom, 0.001)
+                calls += 1
+                torch.cuda.synchronize()
+                compare(from_dev(model), me, "bf16", what=f"mp model L={L} {dt} {family} r{rank}")
+                compare(from_dev(wm)[off:off + ln], we[off:off + ln], "f32", what="mp master")
+                compare(from_dev(vm)[off:off + ln], ve[off:off + ln], "f32", what="mp v")
+                w2, v2 = to_dev(w0, dev=dev), to_dev(v0, dev=dev)
+                gdraa.gdraa_register(w2)
+                gdraa.gdraa_sgd_step_ex(w2, g, v2, lr, mom, 0.001)
+                calls += 1
+                torch.cuda.synchronize()
+                compare(from_dev(w2), we, "f32", what=f"ex w L={L} {dt} {family} r{rank}")
+                compare(from_dev(v2)[off:off + ln], ve[off:off + ln], "f32", what="ex v")
+                for t in (model, w2):
+                    gdraa.gdraa_deregister(t)
                 for t in (buf, w, g):
                     gdraa.gdraa_deregister(t)
                 report["cases"] += 1

@@ -325,3 +325,82 @@ def test_counters_conservation(L, N):
     assert sum(c["ag_sent"] for c in cs) == sum(c["ag_recv"] for c in cs)
     assert sum(c["adds"] + c["divides"] for c in cs) == N * L
     assert all(c["sync_waits"] == (2 if N > 1 else 0) for c in cs)
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT-1: weight decay ("weight decay is 0.001"), the bf16 model copy of the
+# mixed-precision all-gather, and the "poly" learning-rate policy.
+# ---------------------------------------------------------------------------------------
+
+def test_sgd_wd_zero_is_core_update():
+    # wd = 0 forms no decay term: bitwise the pinned core update (incl. -0.0 handling)
+    N, L = 4, 5000
+    gs = [synth.grad_like(41, p, L) for p in range(N)]
+    w0, v0 = synth.w_like(41, L), synth.w_like(42, L)
+    w1, v1 = oracle.sgd_step(gs, w0, v0, 0.1, 0.9)
+    w2, v2 = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, 0.0)
+    assert np.array_equal(w1.view(np.uint32), w2.view(np.uint32))
+    assert np.array_equal(v1.view(np.uint32), v2.view(np.uint32))
+
+
+def test_sgd_wd_dyadic_closed_form():
+    # S:412 v <- mu v + (g + lambda w); w <- w - lr v with dyadic mu = lr = lambda = 1/2,
+    # 1/4, 1/2: every value is exact, so the float trajectory equals the rational one.
+    mu, lr, lam = Fraction(1, 2), Fraction(1, 4), Fraction(1, 2)
+    for N in (1, 2, 4):
+        w, v = _one(1.0), _one(0.0)
+        wk, vk = Fraction(1), Fraction(0)
+        for k in range(5):      # the rational trajectory outgrows 24 bits after ~6 steps
+            w, v = oracle.sgd_step_wd([_one(1.0)] * N, w, v, float(lr), float(mu), float(lam))
+            vk = mu * vk + (1 + lam * wk)
+            wk = wk - lr * vk
+            assert exact(fraction_to_f32(vk)) == vk and exact(fraction_to_f32(wk)) == wk
+            assert exact(v[0]) == vk and exact(w[0]) == wk, (N, k)
+    # first two steps by hand: v1 = 1.5, w1 = 0.625; v2 = 2.0625, w2 = 0.109375
+    w, v = oracle.sgd_step_wd([_one(1.0)], _one(1.0), _one(0.0), 0.25, 0.5, 0.5)
+    assert (float(v[0]), float(w[0])) == (1.5, 0.625)
+    w, v = oracle.sgd_step_wd([_one(1.0)], w, v, 0.25, 0.5, 0.5)
+    assert (float(v[0]), float(w[0])) == (2.0625, 0.109375)
+
+
+@pytest.mark.parametrize("N", [1, 2, 4, 8])
+def test_sgd_wd_integer_family_exact(N):
+    # integer family with lambda = 2^-4: every intermediate stays exactly representable
+    L = 3000
+    gs = [synth.grad_integer(13, p, L) for p in range(N)]
+    w0, v0 = synth.w_integer(13, L), synth.v_integer(13, L)
+    lr, mom, lam = synth.INT_LR, synth.INT_MOM, 2.0**-4
+    w, v = oracle.sgd_step_wd(gs, w0, v0, lr, mom, lam)
+    for i in range(0, L, 11):
+        m = sum(exact(g[i]) for g in gs) / N
+        ge = m + Fraction(lam) * exact(w0[i])
+        vn = Fraction(mom) * exact(v0[i]) + ge
+        wn = exact(w0[i]) - Fraction(lr) * vn
+        assert exact(fraction_to_f32(vn)) == vn and exact(fraction_to_f32(wn)) == wn
+        assert exact(v[i]) == vn and exact(w[i]) == wn, i
+
+
+def test_sgd_mp_model_copy_is_bf16_of_master():
+    # the broadcast model copy is bf16 RNE of the updated fp32 master (torch's cast)
+    N, L = 3, 4000
+    gs = [synth.to_bf16_bits_trunc(synth.grad_like(51, p, L)) for p in range(N)]
+    w0, v0 = synth.w_like(51, L), synth.w_like(52, L)
+    w, v, model = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, 0.001, model_dtype=oracle.BF16)
+    ref = torch.from_numpy(w).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(model, ref)
+    w2, v2 = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, 0.001)
+    assert np.array_equal(w.view(np.uint32), w2.view(np.uint32))
+    w3, v3, m3 = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, 0.001, model_dtype=oracle.F32)
+    assert np.array_equal(m3.view(np.uint32), w.view(np.uint32))
+
+
+def test_poly_lr(golden):
+    for ex in golden["poly_lr"]:
+        assert oracle.poly_lr(ex["lr0"], ex["iter"], ex["max_iter"], ex["power"]) == \
+            np.float32(ex["lr"]), ex["cite"]
+    assert oracle.poly_lr(0.1, 0, 1000, 1.0) == np.float32(0.1)
+    assert oracle.poly_lr(0.1, 1000, 1000, 1.0) == 0.0
+    assert oracle.poly_lr(0.1, 500, 1000, 2.0) == np.float32(0.025)
+    # monotone non-increasing in iter for power > 0
+    lrs = [oracle.poly_lr(0.1, i, 997, 1.0) for i in range(0, 998, 7)]
+    assert all(a >= b for a, b in zip(lrs, lrs[1:]))
