@@ -116,3 +116,53 @@ def test_multiprocess_parity(tmp_path):
     for r in range(world):
         rep = json.load(open(tmp_path / f"rank{r}.json"))
         assert rep["cases"] == len(L_list) * 4
+
+
+def _ls_worker(rank, world, sock, out_dir):
+    """NEXT-4 over real processes: each rank computes its own b-sample least-squares
+    gradient and steps through gdraa_sgd_step; rank 0 checks the serial trajectory."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_1802_02326_b200 import gdraa
+    from synth.least_squares import Problem
+    from tests.test_gpu_training import serial_trajectory
+
+    torch.cuda.set_device(rank)
+    dev = f"cuda:{rank}"
+    os.environ["GDRAA_JOBSERVER"] = sock
+    gdraa.gdraa_init(world, rank)
+    P = Problem(seed=5)
+    b, lr, mom, iters = 8, 0.05, 0.9, 100
+    ref = serial_trajectory(P, iters, world, b, lr, mom)
+    w = torch.zeros(P.d, device=dev)
+    g = torch.zeros(P.d, device=dev)
+    v = torch.zeros(P.d, device=dev)
+    gdraa.gdraa_register(w)
+    gdraa.gdraa_register(g)
+    gap = 0.0
+    for it in range(iters):
+        X, y = P.batch(it, world, b, rank=rank)
+        Xt = torch.from_numpy(X.astype(np.float32)).to(dev)
+        yt = torch.from_numpy(y.astype(np.float32)).to(dev)
+        g.copy_(Xt.T @ (Xt @ w - yt) / b)
+        gdraa.gdraa_sgd_step(w, g, v, lr, mom)
+        gap = max(gap, float(np.max(np.abs(w.cpu().numpy() - ref[it]))))
+    final = w.cpu().numpy()
+    gdraa.gdraa_finalize()
+    with open(os.path.join(out_dir, f"ls{rank}.json"), "w") as f:
+        json.dump({"gap": gap, "w": final.view(np.uint32).tolist()}, f)
+
+
+def test_multiprocess_least_squares_ssgd(tmp_path):
+    from paper_1802_02326_b200 import jobserver
+    world = min(torch.cuda.device_count(), 8)
+    sock = str(tmp_path / "js.sock")
+    js = jobserver.start(world, sock)
+    try:
+        mp.start_processes(_ls_worker, args=(world, sock, str(tmp_path)), nprocs=world,
+                           join=True, start_method="spawn")
+    finally:
+        js.communicate(timeout=120)
+    reps = [json.load(open(tmp_path / f"ls{r}.json")) for r in range(world)]
+    assert all(r["gap"] < 1e-5 for r in reps), [r["gap"] for r in reps]
+    assert all(r["w"] == reps[0]["w"] for r in reps)      # bitwise identical replicas
