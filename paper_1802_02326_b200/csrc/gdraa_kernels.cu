@@ -22,6 +22,7 @@
 // Tensor cores are not used: there is no contraction on this path.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "gdraa_internal.h"
@@ -209,6 +210,9 @@ gdraa_kernel(const __grid_constant__ KParams p) {
 
     // All CTAs read the epoch before any of them can arrive at the exit counter, and the
     // last CTA updates it only after every CTA arrived: one consistent value per call.
+    // Programmatic dependent launch: this grid may have been scheduled while the previous
+    // kernel on the stream was finishing; wait for its completion (a no-op otherwise).
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint64_t epoch = *reinterpret_cast<volatile uint64_t *>(&mine->epoch) + 1;
     if (threadIdx.x == 0) s_abort = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(0);
@@ -371,6 +375,9 @@ gdraa_kernel(const __grid_constant__ KParams p) {
     // a7: "1st synchronization" -- our pushes are performed system-wide, then the last
     // CTA of this rank tells every peer and waits until every peer has done the same.
     if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(2);
+    // Let the next kernel on the stream start launching; it waits for our completion
+    // (griddepcontrol.wait above) before touching anything.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (WORLD > 1) fence_acq_rel_sys();   // N = 1: the kernel boundary orders our stores
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -504,8 +511,23 @@ cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows, boo
         return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(l.fn), grid, block,
                                            args, 0, s);
     }
-    l.fn<<<grid, block, 0, s>>>(p);
-    return cudaGetLastError();
+    // Programmatic stream serialization hides the launch gap between back-to-back
+    // collectives (GDRAA_PDL=0 launches plainly).
+    static const bool pdl = [] {
+        const char *e = std::getenv("GDRAA_PDL");
+        return e == nullptr || e[0] != '0';
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, l.fn, p);
 }
 
 }  // namespace gdraa

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--min-log2", type=int, default=10)
     ap.add_argument("--max-log2", type=int, default=30)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays")
     args = ap.parse_args()
     out = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
@@ -45,12 +46,23 @@ def main():
     lines = []
 
     def timed(fn, iters):
+        """Per-call device time (max over ranks).  With --graph the `iters` calls are
+        captured into one CUDA graph and replayed, so host launch cost is excluded."""
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        graph = None
+        if args.graph:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                for _ in range(iters):
+                    fn()
         dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(iters):
-            fn()
+        if graph is not None:
+            graph.replay()
+        else:
+            for _ in range(iters):
+                fn()
         e1.record(stream)
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1) / iters], device=dev)
@@ -74,6 +86,7 @@ def main():
         gdraa.gdraa_deregister(ours)
         bus = lambda ms: 2 * (world - 1) / world * nbytes / (ms * 1e-3) / 1e9  # noqa: E731
         line = {"n_gpus": world, "bytes": nbytes, "iters": iters,
+                "timing": "cuda_graph_replay" if args.graph else "eager_python_loop",
                 "gdraa_us": t_ours * 1e3, "gdraa_busbw_gbs": bus(t_ours),
                 "nccl_us": t_nccl * 1e3, "nccl_busbw_gbs": bus(t_nccl),
                 "speedup_vs_nccl": t_nccl / t_ours, "max_rel_diff_vs_nccl": rel}
