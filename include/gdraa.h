@@ -165,6 +165,18 @@ float gdraa_poly_lr(float lr0, uint64_t iter, uint64_t max_iter, float power);
  */
 int gdraa_shard(int world, int rank, size_t n, size_t *off, size_t *len);
 
+/*
+ * gdraa_small_message_bytes -- the largest gdraa_allreduce_mean payload (n * element
+ * size, bytes per rank) served by the small-message path at this world size (SURVEY
+ * §8(f) NEXT-2): every rank pushes its whole buffer to every peer as 16-byte entries
+ * that carry the call's epoch flag, so the data's arrival is its own synchronisation
+ * and no device barrier runs; the fold order and rounding -- hence the result, bit for
+ * bit -- are those of the two-shot kernel.  Default 4 MiB / (world - 1) (measured
+ * crossover); GDRAA_LL_MAX_BYTES overrides it, 0 disables the path.  Returns 0 for
+ * world == 1 or out of range.  Pure host function.
+ */
+size_t gdraa_small_message_bytes(int world);
+
 typedef struct {
     uint64_t calls;            /* collective calls completed on the device (device counter) */
     uint64_t sync_waits;       /* device barrier completions: 2 per call when world >= 2     */
@@ -175,6 +187,10 @@ typedef struct {
     uint64_t adds;             /* aggregation adds (Eq. 3, first term)                       */
     uint64_t divides;          /* aggregation divides (Eq. 3, second term)                   */
     uint64_t launches;         /* kernels launched by this library                           */
+    uint64_t ll_calls;         /* allreduce_mean calls served by the small-message path, whose
+                                  synchronisation travels with the data (no device barrier;
+                                  not counted in sync_waits; GDRAA_LL_MAX_BYTES, default
+                                  262144, 0 disables)                                        */
 } gdraa_stats_t;
 
 /*

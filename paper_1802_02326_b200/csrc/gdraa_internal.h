@@ -27,7 +27,8 @@ struct alignas(128) Pad {
     uint64_t sync_waits;
     uint32_t arrive;               // CTA arrival counter of the running call
     uint32_t next;                 // next work chunk of the running call (dynamic schedule)
-    uint64_t _p3[12];
+    uint64_t ll_calls;             // calls served by the small-message (LL) path
+    uint64_t _p3[11];
 };
 static_assert(sizeof(Pad) % 128 == 0, "pad layout");
 
@@ -55,6 +56,10 @@ struct KParams {
     float *v[kMaxWorld];                     // [vr]: local momentum buffer
     float *wm[kMaxWorld];                    // [vr]: local fp32 master weights (kSgdMp)
     Pad *pad[kMaxWorld][kMaxWorld];          // [vr][p]: rank p's pad seen from vr
+    // Small-message path (kMean only): rank p's LL receive buffer seen from vr, laid out
+    // [2 parities][world senders][ll_pairs] x uint4 {word0, flag, word1, flag}.
+    uint4 *ll[kMaxWorld][kMaxWorld];
+    uint64_t ll_pairs;                       // capacity in 8-byte payload pairs per sender
     ErrBlock *err;                           // host-mapped (device alias)
     volatile uint64_t *done[kMaxWorld];      // host-mapped done flags (device alias) or null
 #ifdef GDRAA_TRACE
@@ -74,5 +79,17 @@ cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows,
 
 // Max co-resident CTAs of the kernel for (dtype, mode, world) on this device.
 int max_ctas(int dtype, int mode, int world);
+
+// Small-message allreduce_mean ("LL": data carries its own epoch flags, no barriers).
+// Requires n * elem_size <= 8 * p.ll_pairs.
+cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool cooperative,
+                            cudaStream_t s);
+
+// Largest allreduce_mean payload (bytes per rank) served by the LL path: the measured
+// crossover with the two-shot kernel is ~4 MiB at N=2 and ~1.5 MiB at N=4
+// (profiles/r15_sweep*_ll*.jsonl), i.e. ~4 MiB / (N-1) as the LL bytes grow with N-1.
+// GDRAA_LL_MAX_BYTES overrides it (0 disables the LL path).
+uint64_t ll_limit_bytes(int world);
+constexpr uint64_t kLLBaseBytes = 4ull << 20;
 
 }  // namespace gdraa

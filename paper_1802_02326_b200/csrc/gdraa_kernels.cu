@@ -412,6 +412,186 @@ gdraa_kernel(const __grid_constant__ KParams p) {
 }
 
 // ---------------------------------------------------------------------------------
+// Small-message allreduce_mean (the latency path).  Below ~256 KiB
+// the two device barriers and the pull round trip dominate, so every rank PUSHES its
+// whole buffer into every peer's receive slot as 16-byte entries {word, flag, word, flag}
+// ("LL" format: the epoch flag travels with the data, so the data's arrival is its own
+// 2nd synchronization), then folds the N contributions in ascending rank and divides
+// once -- bitwise the same result as the two-shot kernel (and the oracle).  Receive slots
+// alternate by epoch parity: a rank cannot overwrite slot parity e before every peer
+// finished call e-2, so no exit barrier is needed (the 1st synchronization is implied by
+// the next call's data).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ void st_ll(uint4 *p, uint4 v) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 ld_ll(const uint4 *p) {
+    uint4 r;
+    asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+
+// 8 payload bytes of the buffer at pair j (fewer at the ragged end; the rest is 0).
+__device__ __forceinline__ uint2 load_pair(const void *buf, uint64_t j, uint64_t nbytes) {
+    const uint64_t b0 = j * 8;
+    if (b0 + 8 <= nbytes) return *reinterpret_cast<const uint2 *>(static_cast<const char *>(buf) + b0);
+    uint32_t w[2] = {0u, 0u};
+    const uint16_t *h = static_cast<const uint16_t *>(buf);   // n*s is a multiple of 2
+    for (uint64_t b = b0; b < nbytes; b += 2) {
+        const uint32_t k = static_cast<uint32_t>((b - b0) / 2);
+        w[k / 2] |= static_cast<uint32_t>(h[b / 2]) << (16 * (k % 2));
+    }
+    return make_uint2(w[0], w[1]);
+}
+__device__ __forceinline__ void store_pair(void *buf, uint64_t j, uint64_t nbytes, uint2 v) {
+    const uint64_t b0 = j * 8;
+    if (b0 + 8 <= nbytes) {
+        *reinterpret_cast<uint2 *>(static_cast<char *>(buf) + b0) = v;
+        return;
+    }
+    const uint32_t w[2] = {v.x, v.y};
+    uint16_t *h = static_cast<uint16_t *>(buf);
+    for (uint64_t b = b0; b < nbytes; b += 2) {
+        const uint32_t k = static_cast<uint32_t>((b - b0) / 2);
+        h[b / 2] = static_cast<uint16_t>(w[k / 2] >> (16 * (k % 2)));
+    }
+}
+
+// Fold one 32-bit word position across ranks: one fp32 element or two bf16 elements.
+template <typename TG, int WORLD> struct WordMean;
+template <int WORLD> struct WordMean<float, WORLD> {
+    __device__ __forceinline__ static uint32_t run(const uint32_t (&x)[WORLD]) {
+        float c[WORLD];
+#pragma unroll
+        for (int q = 0; q < WORLD; ++q) c[q] = __uint_as_float(x[q]);
+        return __float_as_uint(average<WORLD>(c));
+    }
+};
+template <int WORLD> struct WordMean<__nv_bfloat16, WORLD> {
+    __device__ __forceinline__ static uint32_t run(const uint32_t (&x)[WORLD]) {
+        float lo[WORLD], hi[WORLD];
+#pragma unroll
+        for (int q = 0; q < WORLD; ++q) {
+            lo[q] = Elem<__nv_bfloat16>::lo(x[q]);
+            hi[q] = Elem<__nv_bfloat16>::hi(x[q]);
+        }
+        return Elem<__nv_bfloat16>::pack(average<WORLD>(lo), average<WORLD>(hi));
+    }
+};
+
+template <typename TG, int WORLD>
+__global__ void __launch_bounds__(512)
+gdraa_ll_kernel(const __grid_constant__ KParams p) {
+    const int vr = blockIdx.y;
+    const int rank = p.rank0 + vr;
+    Pad *mine = p.pad[vr][rank];
+    __shared__ int s_last;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint64_t epoch = *reinterpret_cast<volatile uint64_t *>(&mine->epoch) + 1;
+    const uint32_t flag = static_cast<uint32_t>(epoch);
+    const uint64_t par = epoch & 1u;
+    const uint64_t nbytes = p.n * sizeof(TG);
+    const uint64_t npairs = (nbytes + 7) / 8;
+    void *const buf = p.dst[vr][rank];
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    bool ok = true;
+    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < npairs;
+         j += stride) {
+        const uint2 mine_pair = load_pair(buf, j, nbytes);
+        const uint4 entry = make_uint4(mine_pair.x, flag, mine_pair.y, flag);
+#pragma unroll
+        for (int k = 1; k < WORLD; ++k) {   // push to every peer's slot [par][rank]
+            const int q = (rank + k) % WORLD;
+            st_ll(p.ll[vr][q] + (par * WORLD + rank) * p.ll_pairs + j, entry);
+        }
+        uint32_t w0[WORLD], w1[WORLD];
+#pragma unroll
+        for (int q = 0; q < WORLD; ++q) {
+            if (q == rank) {
+                w0[q] = mine_pair.x;
+                w1[q] = mine_pair.y;
+                continue;
+            }
+            const uint4 *src = p.ll[vr][rank] + (par * WORLD + q) * p.ll_pairs + j;
+            uint4 r = ld_ll(src);
+            if (r.y != flag || r.w != flag) {
+                const uint64_t t0 = global_timer_ns();
+                do {
+                    r = ld_ll(src);
+                    if (global_timer_ns() - t0 > p.timeout_ns) {
+                        report_timeout(p.err, 1, q, vr);
+                        ok = false;
+                        break;
+                    }
+                } while (r.y != flag || r.w != flag);
+            }
+            w0[q] = r.x;
+            w1[q] = r.z;
+        }
+        if (!ok) break;
+        store_pair(buf, j, nbytes,
+                   make_uint2(WordMean<TG, WORLD>::run(w0), WordMean<TG, WORLD>::run(w1)));
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&mine->arrive, 1u);
+        s_last = (prev == gridDim.x - 1);
+        if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        mine->arrive = 0;
+        mine->calls += 1;
+        mine->ll_calls += 1;
+        mine->epoch = epoch;
+        if (p.done[vr] != nullptr) *p.done[vr] = epoch;
+    }
+}
+
+using KernelFnLL = void (*)(KParams);
+
+// Programmatic stream serialization hides the launch gap between back-to-back
+// collectives (GDRAA_PDL=0 launches plainly).
+cudaError_t launch_pdl(void (*fn)(KParams), dim3 grid, dim3 block, cudaStream_t s,
+                       const KParams &p) {
+    static const bool pdl = [] {
+        const char *e = std::getenv("GDRAA_PDL");
+        return e == nullptr || e[0] != '0';
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fn, p);
+}
+
+template <typename TG>
+KernelFnLL pick_ll_t(int world) {
+    switch (world) {
+        case 2: return gdraa_ll_kernel<TG, 2>;
+        case 3: return gdraa_ll_kernel<TG, 3>;
+        case 4: return gdraa_ll_kernel<TG, 4>;
+        case 5: return gdraa_ll_kernel<TG, 5>;
+        case 6: return gdraa_ll_kernel<TG, 6>;
+        case 7: return gdraa_ll_kernel<TG, 7>;
+        case 8: return gdraa_ll_kernel<TG, 8>;
+        default: return nullptr;
+    }
+}
+
+// ---------------------------------------------------------------------------------
 // Launch shapes (measured on B200): vectors in flight per
 // thread U, CTA size and CTAs per SM.
 // ---------------------------------------------------------------------------------
@@ -511,23 +691,32 @@ cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows, boo
         return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(l.fn), grid, block,
                                            args, 0, s);
     }
-    // Programmatic stream serialization hides the launch gap between back-to-back
-    // collectives (GDRAA_PDL=0 launches plainly).
-    static const bool pdl = [] {
-        const char *e = std::getenv("GDRAA_PDL");
-        return e == nullptr || e[0] != '0';
-    }();
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, l.fn, p);
+    return launch_pdl(l.fn, grid, block, s, p);
+}
+
+cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool cooperative,
+                            cudaStream_t s) {
+    KernelFnLL fn = dtype == GDRAA_F32 ? pick_ll_t<float>(p.world)
+                                       : pick_ll_t<__nv_bfloat16>(p.world);
+    if (fn == nullptr) return cudaErrorInvalidValue;
+    const uint64_t es = dtype == GDRAA_F32 ? 4 : 2;
+    if (p.n * es > 8 * p.ll_pairs) return cudaErrorInvalidValue;
+    constexpr int kT = 512;
+    const uint64_t npairs = (p.n * es + 7) / 8;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint64_t gx = (npairs + kT - 1) / kT;
+    const uint64_t cap = static_cast<uint64_t>(sms) * 2 / vr_rows;   // all resident
+    if (gx > cap) gx = cap;
+    if (gx < 1) gx = 1;
+    dim3 grid(static_cast<unsigned>(gx), vr_rows), block(kT);
+    if (cooperative) {
+        void *args[] = {const_cast<KParams *>(&p)};
+        return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(fn), grid, block, args,
+                                           0, s);
+    }
+    return launch_pdl(fn, grid, block, s, p);
 }
 
 }  // namespace gdraa

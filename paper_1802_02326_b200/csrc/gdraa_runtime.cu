@@ -135,6 +135,9 @@ struct State {
     bool page_owned = false;            // world == 1 without a job server: our own page
     Pad *pad = nullptr;
     Pad *peer_pad[kMaxWorld] = {};
+    uint4 *ll = nullptr;                // small-message receive slots (world > 1)
+    uint4 *peer_ll[kMaxWorld] = {};
+    uint64_t ll_pairs = 0;
     ErrBlock *err_h = nullptr, *err_d = nullptr;
     volatile uint64_t *done_d = nullptr;
     std::vector<Registration> regs;
@@ -325,7 +328,11 @@ void fill_common(KParams &p, uint64_t n) {
     uint64_t off, len;
     partition(n, g.world, g.rank, &p.blk, &off, &len);
     p.timeout_ns = g.timeout_ns;
-    for (int q = 0; q < g.world; ++q) p.pad[0][q] = g.peer_pad[q];
+    for (int q = 0; q < g.world; ++q) {
+        p.pad[0][q] = g.peer_pad[q];
+        p.ll[0][q] = g.peer_ll[q];
+    }
+    p.ll_pairs = g.ll_pairs;
     p.err = g.err_d;
     p.done[0] = g.done_d;
 }
@@ -357,8 +364,23 @@ int launch(const KParams &p, int dtype, int mode, cudaStream_t s) {
 // ---------------------------------------------------------------------------------
 struct VrDevice {
     Pad *pads[kMaxWorld + 1] = {};      // pads[world] -> `world` consecutive Pads
+    uint4 *ll[kMaxWorld + 1] = {};      // ll[world] -> `world` LL receive areas
+    uint64_t ll_pairs[kMaxWorld + 1] = {};
     ErrBlock *err_h = nullptr, *err_d = nullptr;
 };
+
+}  // namespace
+
+uint64_t ll_limit_bytes(int world) {
+    if (world < 2) return 0;
+    const uint64_t dflt = kLLBaseBytes / static_cast<uint64_t>(world - 1);
+    return env_u64("GDRAA_LL_MAX_BYTES", dflt) / 8 * 8;
+}
+
+namespace {
+
+// One rank's LL receive area: [2 parities][world senders][pairs] x 16 bytes.
+size_t ll_area_bytes(int world, uint64_t pairs) { return 2ull * world * pairs * sizeof(uint4); }
 std::map<int, VrDevice> g_vr;
 
 int vr_prepare(int world, VrDevice **out) {
@@ -386,6 +408,14 @@ int vr_prepare(int world, VrDevice **out) {
         CUDA_TRY(cudaMalloc(&pp, sizeof(Pad) * world));
         CUDA_TRY(cudaMemset(pp, 0, sizeof(Pad) * world));
         d.pads[world] = static_cast<Pad *>(pp);
+    }
+    const uint64_t pairs = ll_limit_bytes(world) / 8;
+    if (world > 1 && pairs > 0 && d.ll[world] == nullptr) {
+        void *lp = nullptr;
+        CUDA_TRY(cudaMalloc(&lp, ll_area_bytes(world, pairs) * world));
+        CUDA_TRY(cudaMemset(lp, 0, ll_area_bytes(world, pairs) * world));
+        d.ll[world] = static_cast<uint4 *>(lp);
+        d.ll_pairs[world] = pairs;
     }
     *out = &d;
     return GDRAA_OK;
@@ -447,11 +477,21 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
             p.src[r][q] = src[q];
             p.dst[r][q] = dst[q];
             p.pad[r][q] = d->pads[world] + q;
+            if (d->ll[world] != nullptr)
+                p.ll[r][q] = d->ll[world] +
+                             q * (ll_area_bytes(world, d->ll_pairs[world]) / sizeof(uint4));
         }
         p.v[r] = upd ? a.v[r] : nullptr;
         p.wm[r] = mode == kSgdMp ? a.wm[r] : nullptr;
     }
     p.err = d->err_d;
+    p.ll_pairs = d->ll[world] != nullptr ? d->ll_pairs[world] : 0;
+    const size_t es = dtype == GDRAA_F32 ? 4 : 2;
+    if (mode == kMean && world > 1 && n * es <= 8 * p.ll_pairs) {   // latency path
+        cudaError_t e = launch_gdraa_ll(p, dtype, world, true, s);
+        if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr LL launch: %s", cudaGetErrorString(e));
+        return GDRAA_OK;
+    }
     int gx = 0;
     cudaError_t e = launch_gdraa(p, dtype, mode, world, true, s, &gx);
     if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr kernel launch: %s", cudaGetErrorString(e));
@@ -468,6 +508,11 @@ extern "C" {
 const char *gdraa_last_error(void) { return t_err.c_str(); }
 
 const char *gdraa_version(void) { return "gdraa 0.1.0 (sm_100a)"; }
+
+size_t gdraa_small_message_bytes(int world) {
+    if (world < 1 || world > kMaxWorld) return 0;
+    return static_cast<size_t>(ll_limit_bytes(world));
+}
 
 int gdraa_shard(int world, int rank, size_t n, size_t *off, size_t *len) {
     if (off == nullptr || len == nullptr) return fail(GDRAA_EINVAL, "null output pointer");
@@ -566,6 +611,22 @@ int gdraa_init(int world, int rank) {
         peers[0] = g.pad;
     }
     for (int p = 0; p < world; ++p) g.peer_pad[p] = static_cast<Pad *>(peers[p]);
+
+    // Small-message receive slots (registration sequence 2): [2][world][pairs] x 16 B.
+    const uint64_t ll_bytes = ll_limit_bytes(world);
+    if (world > 1 && ll_bytes > 0) {
+        g.ll_pairs = ll_bytes / 8;
+        const size_t sz = ll_area_bytes(world, g.ll_pairs);
+        void *lp = nullptr;
+        CUDA_TRY(cudaMalloc(&lp, sz));
+        CUDA_TRY(cudaMemset(lp, 0, sz));
+        CUDA_TRY(cudaDeviceSynchronize());
+        g.ll = static_cast<uint4 *>(lp);
+        void *lpeers[kMaxWorld] = {};
+        int rc = ipc_exchange(g.ll, sz, sz, -2, 2, lpeers);
+        if (rc) return cleanup_fail(rc);
+        for (int p = 0; p < world; ++p) g.peer_ll[p] = static_cast<uint4 *>(lpeers[p]);
+    }
     g.inited = true;
     return GDRAA_OK;
 }
@@ -621,8 +682,16 @@ int gdraa_allreduce_mean(void *buf, gdraa_stream_t s) {
         p.src[0][q] = r->peer[q];
         p.dst[0][q] = r->peer[q];
     }
-    rc = launch(p, r->dtype, kMean, reinterpret_cast<cudaStream_t>(s));
-    if (rc) return rc;
+    if (g.ll != nullptr && r->n * elem_size(r->dtype) <= 8 * g.ll_pairs) {
+        // small message: the latency path (same result, bit for bit)
+        p.dst[0][g.rank] = r->local;
+        cudaError_t e = launch_gdraa_ll(p, r->dtype, 1, false, reinterpret_cast<cudaStream_t>(s));
+        if (e != cudaSuccess) return fail(GDRAA_ECUDA, "LL kernel launch: %s", cudaGetErrorString(e));
+        g.issued += 1;
+    } else {
+        rc = launch(p, r->dtype, kMean, reinterpret_cast<cudaStream_t>(s));
+        if (rc) return rc;
+    }
     account(r->n, r->dtype, 0);
     return GDRAA_OK;
 }
@@ -701,6 +770,7 @@ int gdraa_get_stats(gdraa_stats_t *out) {
     *out = g.host;
     out->calls = host.calls;
     out->sync_waits = host.sync_waits;
+    out->ll_calls = host.ll_calls;
     return GDRAA_OK;
 }
 
@@ -729,6 +799,7 @@ int gdraa_finalize(void) {
     for (auto &kv : g.opened) cudaIpcCloseMemHandle(kv.second);
     g.opened.clear();
     if (g.pad) cudaFree(g.pad);
+    if (g.ll) cudaFree(g.ll);
     if (g.page_registered) cudaHostUnregister(g.page);
     if (g.page) munmap(g.page, 4096);
     if (g.err_h) cudaFreeHost(g.err_h);

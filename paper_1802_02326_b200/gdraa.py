@@ -20,6 +20,7 @@ ERRORS = {0: "GDRAA_OK", -1: "GDRAA_EINVAL", -2: "GDRAA_ENOTREG", -3: "GDRAA_ESH
           -4: "GDRAA_ECUDA", -5: "GDRAA_ETIMEOUT", -6: "GDRAA_ESTATE", -7: "GDRAA_EJOBSERVER"}
 
 EXPORTED = ["gdraa_sgd_step_ex", "gdraa_sgd_step_mp", "gdraa_poly_lr",
+            "gdraa_small_message_bytes",
             "gdraa_vr_sgd_step_ex", "gdraa_vr_sgd_step_mp",
             "gdraa_init", "gdraa_register", "gdraa_deregister","gdraa_allreduce_mean", "gdraa_sgd_step",
             "gdraa_shard", "gdraa_get_stats", "gdraa_finalize", "gdraa_last_error",
@@ -36,7 +37,7 @@ class GdraaError(RuntimeError):
 class gdraa_stats_t(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in
                 ("calls", "sync_waits", "rs_bytes_in", "rs_bytes_out", "ag_bytes_out",
-                 "ag_bytes_in", "adds", "divides", "launches")]
+                 "ag_bytes_in", "adds", "divides", "launches", "ll_calls")]
 
 
 if not os.path.exists(LIB_PATH):
@@ -63,6 +64,7 @@ _sig = {
     "gdraa_sgd_step_ex": ([_vp, _vp, _vp, _f, _f, _f, _vp], _i),
     "gdraa_sgd_step_mp": ([_vp, _vp, _vp, _vp, _f, _f, _f, _vp], _i),
     "gdraa_poly_lr": ([_f, ctypes.c_uint64, ctypes.c_uint64, _f], _f),
+    "gdraa_small_message_bytes": ([_i], _sz),
     "gdraa_vr_sgd_step_ex": ([_i, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                               ctypes.POINTER(_vp), _sz, _i, _f, _f, _f, _vp], _i),
     "gdraa_vr_sgd_step_mp": ([_i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
@@ -152,6 +154,10 @@ def gdraa_sgd_step_mp(w_master, w_model, g, v, lr: float, mom: float, wd: float 
 
 def gdraa_poly_lr(lr0: float, it: int, max_iter: int, power: float = 1.0) -> float:
     return float(_lib.gdraa_poly_lr(lr0, it, max_iter, power))
+
+
+def gdraa_small_message_bytes(world: int) -> int:
+    return int(_lib.gdraa_small_message_bytes(world))
 
 
 def gdraa_shard(world: int, rank: int, n: int):

@@ -95,3 +95,12 @@ def test_poly_lr_matches_oracle(golden):
         for power in (0.5, 1.0, 2.0):
             assert gdraa.gdraa_poly_lr(0.1, it, 4999, power) == oracle.poly_lr(0.1, it, 4999, power)
     assert gdraa.gdraa_poly_lr(0.1, 1, 0, 1.0) == -1.0
+
+
+def test_small_message_threshold():
+    """NEXT-2 latency-path threshold: 4 MiB / (N-1), 8-byte multiple, none at N=1."""
+    assert gdraa.gdraa_small_message_bytes(1) == 0
+    for n in range(2, 9):
+        lim = gdraa.gdraa_small_message_bytes(n)
+        assert lim % 8 == 0 and (4 << 20) // (n - 1) - 8 < lim <= (4 << 20) // (n - 1)
+    assert gdraa.gdraa_small_message_bytes(9) == 0

@@ -72,6 +72,25 @@ def test_vr_allreduce_mean(N, dt, family):
             compare(from_dev(bufs[r]), exp, dt, what=f"mean N={N} L={L} rank {r}")
 
 
+@pytest.mark.parametrize("N", [2, 3, 8])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_vr_allreduce_mean_latency_path(N, dt):
+    """Sizes on both sides of the small-message (LL) threshold, odd bf16 lengths (ragged
+    8-byte pairs), repeated calls (epoch parity of the receive slots)."""
+    bf16 = dt == "bf16"
+    es = 2 if bf16 else 4
+    lim = gdraa.gdraa_small_message_bytes(N) // es      # largest LL element count
+    for L in (1, 2, 3, 4097, 65535, 65536, lim - 1, lim, lim + 1):
+        for it in range(3):
+            gs = make_grads("like", 700 + it, N, L, bf16)
+            exp = oracle.allreduce_mean(gs)
+            bufs = [to_dev(g, bf16) for g in gs]
+            gdraa.gdraa_vr_allreduce_mean(bufs)
+            torch.cuda.synchronize()
+            for r in range(N):
+                compare(from_dev(bufs[r]), exp, dt, what=f"LL mean N={N} L={L} it{it} r{r}")
+
+
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 6, 7, 8])
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
 @pytest.mark.parametrize("family", ["int", "like"])

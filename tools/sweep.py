@@ -41,6 +41,7 @@ def main():
     js = jobserver.setup_for_rank(world, rank, local, tag="sweep" + os.environ["MASTER_PORT"])
     gdraa.gdraa_init(world, rank)
     stream = torch.cuda.current_stream()
+    cap_stream = torch.cuda.Stream()
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     lines = []
@@ -52,7 +53,7 @@ def main():
         graph = None
         if args.graph:
             graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=stream):
+            with torch.cuda.graph(graph, stream=cap_stream):   # fn uses the current stream
                 for _ in range(iters):
                     fn()
         dist.barrier(device_ids=[local])
@@ -81,7 +82,7 @@ def main():
         torch.cuda.synchronize()
         rel = float(((ours - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item())
         iters = 1000 if nbytes <= (1 << 20) else (200 if nbytes <= (1 << 26) else 20)
-        t_ours = timed(lambda: gdraa.gdraa_allreduce_mean(ours, stream), iters)
+        t_ours = timed(lambda: gdraa.gdraa_allreduce_mean(ours), iters)   # current stream
         t_nccl = timed(lambda: dist.all_reduce(ref, op=dist.ReduceOp.AVG), iters)
         gdraa.gdraa_deregister(ours)
         bus = lambda ms: 2 * (world - 1) / world * nbytes / (ms * 1e-3) / 1e9  # noqa: E731
