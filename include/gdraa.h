@@ -150,6 +150,27 @@ int gdraa_sgd_step_mp(float *w_master, void *w_model, const void *g, float *v, f
                       float mom, float wd, gdraa_stream_t s);
 
 /*
+ * Bucketed calls ("synchronizations ... as late as the DL needs",
+ * P:189): the same collectives on the element range [first, first + count) of the
+ * registered buffers, so a caller can reduce and apply each gradient bucket as soon as
+ * the backward pass has produced it, on a side stream, overlapping the rest of the
+ * backward.  Every rank must issue the same sequence of ranges.  The owner partition
+ * (gdraa_shard) applies to the range: rank r owns [first + off_r, first + off_r + len_r)
+ * with off_r/len_r = gdraa_shard(world, r, count) -- so v (and w_master) must be stepped
+ * with the same bucketing every iteration.
+ *   w, g, v, buf, w_master, w_model: the base pointers as registered / allocated.
+ *   first: multiple of 4; count >= 1; first + count <= n.
+ * Errors as the whole-buffer calls, plus EINVAL for a bad range.  GDRAA_MAX_CTAS caps
+ * the CTAs per call so that bucket kernels leave SMs to the concurrent backward.
+ */
+int gdraa_allreduce_mean_range(void *buf, size_t first, size_t count, gdraa_stream_t s);
+int gdraa_sgd_step_range(float *w, const void *g, float *v, size_t first, size_t count,
+                         float lr, float mom, float wd, gdraa_stream_t s);
+int gdraa_sgd_step_mp_range(float *w_master, void *w_model, const void *g, float *v,
+                            size_t first, size_t count, float lr, float mom, float wd,
+                            gdraa_stream_t s);
+
+/*
  * gdraa_poly_lr -- the paper's "poly" learning-rate policy with "gamma is 1" read as
  * the power: lr0 * (1 - iter/max_iter)^power, in double, rounded
  * once to float; 0 for iter >= max_iter; -1 if max_iter == 0.  Pure host function.

@@ -677,7 +677,14 @@ cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows, boo
                          cudaStream_t s, int *grid_x_out) {
     Launch l = pick(dtype, mode, p.world);
     if (l.fn == nullptr) return cudaErrorInvalidValue;
-    const int cap = max_ctas(dtype, mode, p.world) / vr_rows;
+    // GDRAA_MAX_CTAS (tuning only): cap the grid, e.g. to leave SMs to a concurrent
+    // backward pass when buckets are reduced on a side stream (NEXT-3).
+    static const int env_cap = [] {
+        const char *e = std::getenv("GDRAA_MAX_CTAS");
+        return e ? std::atoi(e) : 0;
+    }();
+    int cap = max_ctas(dtype, mode, p.world) / vr_rows;
+    if (env_cap > 0 && env_cap < cap) cap = env_cap;
     if (cap < 1) return cudaErrorInvalidConfiguration;
     const uint64_t nvec = (p.blk + E - 1) / E;
     const uint64_t per_chunk = static_cast<uint64_t>(l.threads) * l.u;

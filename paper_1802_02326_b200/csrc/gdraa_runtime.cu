@@ -668,23 +668,45 @@ int gdraa_deregister(void *buf) {
     return fail(GDRAA_ENOTREG, "buffer %p is not registered", buf);
 }
 
-int gdraa_allreduce_mean(void *buf, gdraa_stream_t s) {
+// Resolve the element range [first, first + count) of a registration (count == SIZE_MAX:
+// the whole buffer).  Ranges start on a 4-element boundary so every vector stays aligned.
+static int resolve_range(const Registration *r, size_t first, size_t *count) {
+    if (*count == SIZE_MAX) {
+        if (first != 0) return fail(GDRAA_EINVAL, "whole-buffer call with first != 0");
+        *count = r->n;
+        return GDRAA_OK;
+    }
+    if (*count == 0) return fail(GDRAA_EINVAL, "count must be >= 1");
+    if (first % 4 != 0) return fail(GDRAA_EINVAL, "first (%zu) must be a multiple of 4", first);
+    if (first > r->n || *count > r->n - first)
+        return fail(GDRAA_EINVAL, "range [%zu, %zu) exceeds the registered %zu elements", first,
+                    first + *count, r->n);
+    return GDRAA_OK;
+}
+
+static void *offset_ptr(void *p, size_t elems, size_t es) {
+    return p == nullptr ? nullptr : static_cast<char *>(p) + elems * es;
+}
+
+static int mean_common(void *buf, size_t first, size_t count, gdraa_stream_t s) {
     std::lock_guard<std::mutex> lk(g_mu);
     int rc = check_sticky();
     if (rc) return rc;
     const Registration *r = find_reg(buf);
     if (r == nullptr) return fail(GDRAA_ENOTREG, "buffer %p is not registered", buf);
+    rc = resolve_range(r, first, &count);
+    if (rc) return rc;
     rc = wait_go();
     if (rc) return rc;
+    const size_t es = elem_size(r->dtype);
     KParams p;
-    fill_common(p, r->n);
+    fill_common(p, count);
     for (int q = 0; q < g.world; ++q) {
-        p.src[0][q] = r->peer[q];
-        p.dst[0][q] = r->peer[q];
+        p.src[0][q] = offset_ptr(r->peer[q], first, es);
+        p.dst[0][q] = offset_ptr(r->peer[q], first, es);
     }
-    if (g.ll != nullptr && r->n * elem_size(r->dtype) <= 8 * g.ll_pairs) {
+    if (g.ll != nullptr && count * es <= 8 * g.ll_pairs) {
         // small message: the latency path (same result, bit for bit)
-        p.dst[0][g.rank] = r->local;
         cudaError_t e = launch_gdraa_ll(p, r->dtype, 1, false, reinterpret_cast<cudaStream_t>(s));
         if (e != cudaSuccess) return fail(GDRAA_ECUDA, "LL kernel launch: %s", cudaGetErrorString(e));
         g.issued += 1;
@@ -692,14 +714,22 @@ int gdraa_allreduce_mean(void *buf, gdraa_stream_t s) {
         rc = launch(p, r->dtype, kMean, reinterpret_cast<cudaStream_t>(s));
         if (rc) return rc;
     }
-    account(r->n, r->dtype, 0);
+    account(count, r->dtype, 0);
     return GDRAA_OK;
 }
 
-// Shared body of gdraa_sgd_step / _ex (mode kSgd: dst = replicated fp32 w) and
-// gdraa_sgd_step_mp (mode kSgdMp: dst = replicated bf16 model copy, wm = local master).
-static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, float lr,
-                      float mom, float wd, gdraa_stream_t s) {
+int gdraa_allreduce_mean(void *buf, gdraa_stream_t s) { return mean_common(buf, 0, SIZE_MAX, s); }
+
+int gdraa_allreduce_mean_range(void *buf, size_t first, size_t count, gdraa_stream_t s) {
+    if (count == SIZE_MAX) return fail(GDRAA_EINVAL, "count out of range");
+    return mean_common(buf, first, count, s);
+}
+
+// Shared body of gdraa_sgd_step / _ex / _range (mode kSgd: dst = replicated fp32 w) and
+// gdraa_sgd_step_mp / _mp_range (mode kSgdMp: dst = replicated bf16 model copy, wm =
+// local master), on the element range [first, first + count) (SIZE_MAX: everything).
+static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, size_t first,
+                      size_t count, float lr, float mom, float wd, gdraa_stream_t s) {
     std::lock_guard<std::mutex> lk(g_mu);
     int rc = check_sticky();
     if (rc) return rc;
@@ -720,37 +750,53 @@ static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, 
     if (v == nullptr || !aligned16(v)) return fail(GDRAA_EINVAL, "v is null or not 16-byte aligned");
     if (mode == kSgdMp && (wm == nullptr || !aligned16(wm)))
         return fail(GDRAA_EINVAL, "w_master is null or not 16-byte aligned");
+    rc = resolve_range(rw, first, &count);
+    if (rc) return rc;
     rc = wait_go();
     if (rc) return rc;
+    const size_t eg = elem_size(rg->dtype), ew = elem_size(rw->dtype);
     KParams p;
-    fill_common(p, rw->n);
+    fill_common(p, count);
     p.lr = lr;
     p.mom = mom;
     p.wd = wd;
     for (int q = 0; q < g.world; ++q) {
-        p.src[0][q] = rg->peer[q];
-        p.dst[0][q] = rw->peer[q];
+        p.src[0][q] = offset_ptr(rg->peer[q], first, eg);
+        p.dst[0][q] = offset_ptr(rw->peer[q], first, ew);
     }
-    p.v[0] = v;
-    p.wm[0] = mode == kSgdMp ? wm : nullptr;
+    p.v[0] = static_cast<float *>(offset_ptr(v, first, 4));
+    p.wm[0] = mode == kSgdMp ? static_cast<float *>(offset_ptr(wm, first, 4)) : nullptr;
     rc = launch(p, rg->dtype, mode, reinterpret_cast<cudaStream_t>(s));
     if (rc) return rc;
-    account(rw->n, rg->dtype, mode == kSgd ? 4 : 2);
+    account(count, rg->dtype, mode == kSgd ? 4 : 2);
     return GDRAA_OK;
 }
 
 int gdraa_sgd_step(float *w, const void *gr, float *v, float lr, float mom, gdraa_stream_t s) {
-    return sgd_common(kSgd, nullptr, w, gr, v, lr, mom, 0.0f, s);
+    return sgd_common(kSgd, nullptr, w, gr, v, 0, SIZE_MAX, lr, mom, 0.0f, s);
 }
 
 int gdraa_sgd_step_ex(float *w, const void *gr, float *v, float lr, float mom, float wd,
                       gdraa_stream_t s) {
-    return sgd_common(kSgd, nullptr, w, gr, v, lr, mom, wd, s);
+    return sgd_common(kSgd, nullptr, w, gr, v, 0, SIZE_MAX, lr, mom, wd, s);
 }
 
 int gdraa_sgd_step_mp(float *w_master, void *w_model, const void *gr, float *v, float lr,
                       float mom, float wd, gdraa_stream_t s) {
-    return sgd_common(kSgdMp, w_master, w_model, gr, v, lr, mom, wd, s);
+    return sgd_common(kSgdMp, w_master, w_model, gr, v, 0, SIZE_MAX, lr, mom, wd, s);
+}
+
+int gdraa_sgd_step_range(float *w, const void *gr, float *v, size_t first, size_t count,
+                         float lr, float mom, float wd, gdraa_stream_t s) {
+    if (count == SIZE_MAX) return fail(GDRAA_EINVAL, "count out of range");
+    return sgd_common(kSgd, nullptr, w, gr, v, first, count, lr, mom, wd, s);
+}
+
+int gdraa_sgd_step_mp_range(float *w_master, void *w_model, const void *gr, float *v,
+                            size_t first, size_t count, float lr, float mom, float wd,
+                            gdraa_stream_t s) {
+    if (count == SIZE_MAX) return fail(GDRAA_EINVAL, "count out of range");
+    return sgd_common(kSgdMp, w_master, w_model, gr, v, first, count, lr, mom, wd, s);
 }
 
 float gdraa_poly_lr(float lr0, uint64_t iter, uint64_t max_iter, float power) {

@@ -20,7 +20,8 @@ ERRORS = {0: "GDRAA_OK", -1: "GDRAA_EINVAL", -2: "GDRAA_ENOTREG", -3: "GDRAA_ESH
           -4: "GDRAA_ECUDA", -5: "GDRAA_ETIMEOUT", -6: "GDRAA_ESTATE", -7: "GDRAA_EJOBSERVER"}
 
 EXPORTED = ["gdraa_sgd_step_ex", "gdraa_sgd_step_mp", "gdraa_poly_lr",
-            "gdraa_small_message_bytes",
+            "gdraa_small_message_bytes", "gdraa_allreduce_mean_range",
+            "gdraa_sgd_step_range", "gdraa_sgd_step_mp_range",
             "gdraa_vr_sgd_step_ex", "gdraa_vr_sgd_step_mp",
             "gdraa_init", "gdraa_register", "gdraa_deregister","gdraa_allreduce_mean", "gdraa_sgd_step",
             "gdraa_shard", "gdraa_get_stats", "gdraa_finalize", "gdraa_last_error",
@@ -65,6 +66,9 @@ _sig = {
     "gdraa_sgd_step_mp": ([_vp, _vp, _vp, _vp, _f, _f, _f, _vp], _i),
     "gdraa_poly_lr": ([_f, ctypes.c_uint64, ctypes.c_uint64, _f], _f),
     "gdraa_small_message_bytes": ([_i], _sz),
+    "gdraa_allreduce_mean_range": ([_vp, _sz, _sz, _vp], _i),
+    "gdraa_sgd_step_range": ([_vp, _vp, _vp, _sz, _sz, _f, _f, _f, _vp], _i),
+    "gdraa_sgd_step_mp_range": ([_vp, _vp, _vp, _vp, _sz, _sz, _f, _f, _f, _vp], _i),
     "gdraa_vr_sgd_step_ex": ([_i, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                               ctypes.POINTER(_vp), _sz, _i, _f, _f, _f, _vp], _i),
     "gdraa_vr_sgd_step_mp": ([_i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
@@ -154,6 +158,24 @@ def gdraa_sgd_step_mp(w_master, w_model, g, v, lr: float, mom: float, wd: float 
 
 def gdraa_poly_lr(lr0: float, it: int, max_iter: int, power: float = 1.0) -> float:
     return float(_lib.gdraa_poly_lr(lr0, it, max_iter, power))
+
+
+def gdraa_allreduce_mean_range(buf, first: int, count: int, stream=None):
+    _check(_lib.gdraa_allreduce_mean_range(_ptr(buf), first, count, _stream(stream)),
+           "gdraa_allreduce_mean_range")
+
+
+def gdraa_sgd_step_range(w, g, v, first: int, count: int, lr: float, mom: float,
+                         wd: float = 0.0, stream=None):
+    _check(_lib.gdraa_sgd_step_range(_ptr(w), _ptr(g), _ptr(v), first, count, lr, mom, wd,
+                                     _stream(stream)), "gdraa_sgd_step_range")
+
+
+def gdraa_sgd_step_mp_range(w_master, w_model, g, v, first: int, count: int, lr: float,
+                            mom: float, wd: float = 0.0, stream=None):
+    _check(_lib.gdraa_sgd_step_mp_range(_ptr(w_master), _ptr(w_model), _ptr(g), _ptr(v), first,
+                                        count, lr, mom, wd, _stream(stream)),
+           "gdraa_sgd_step_mp_range")
 
 
 def gdraa_small_message_bytes(world: int) -> int:

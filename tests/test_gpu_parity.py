@@ -228,6 +228,26 @@ def test_world1_sgd_and_mean(world1, dt):
     assert st["calls"] == 4 and st["launches"] == 4 and st["sync_waits"] == 0, st
 
 
+def test_world1_bucketed_ranges(world1):
+    """NEXT-3 range calls at world 1: buckets stepped out of order equal one full step."""
+    L = 300_008
+    gs = make_grads("like", 12, 1, L, False)
+    w0, v0 = synth.w_like(12, L), synth.w_like(13, L)
+    w_exp, v_exp = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, 0.001)
+    g, w, v = to_dev(gs[0]), to_dev(w0), to_dev(v0)
+    gdraa.gdraa_register(w)
+    gdraa.gdraa_register(g)
+    for first, count in [(200_000, 100_008), (4, 199_996), (0, 4)]:
+        gdraa.gdraa_sgd_step_range(w, g, v, first, count, 0.1, 0.9, 0.001)
+    torch.cuda.synchronize()
+    compare(from_dev(w), w_exp, "f32", what="w")
+    compare(from_dev(v), v_exp, "f32", what="v")
+    for bad in [(1, 10), (0, 0), (300_000, 9), (400_000, 4)]:
+        with pytest.raises(gdraa.GdraaError) as e:
+            gdraa.gdraa_sgd_step_range(w, g, v, bad[0], bad[1], 0.1, 0.9)
+        assert e.value.name == "GDRAA_EINVAL", bad
+
+
 def test_world1_errors(world1):
     a = torch.zeros(1000, device=DEV)
     b = torch.zeros(1000, device=DEV)

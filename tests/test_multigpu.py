@@ -123,6 +123,75 @@ def test_multiprocess_parity(tmp_path):
         assert rep["cases"] == len(L_list) * 4
 
 
+BUCKETS = [(600_000, 400_004), (0, 600_000), (1_000_004, 48_572)]   # backward order
+
+
+def _bucket_worker(rank, world, sock, out_dir):
+    """NEXT-3: the gradient buffer reduced and applied bucket by bucket (last layers
+    first, as a backward pass produces them) on a side stream; w must equal the
+    whole-buffer oracle step and v the oracle on every rank's per-bucket shards."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    import synth
+    from paper_1802_02326_b200 import gdraa
+    from tests._parity import compare
+    from tests.test_gpu_parity import from_dev, make_grads, to_dev
+
+    torch.cuda.set_device(rank)
+    dev = f"cuda:{rank}"
+    os.environ["GDRAA_JOBSERVER"] = sock
+    gdraa.gdraa_init(world, rank)
+    L = 1_048_576
+    side = torch.cuda.Stream()
+    for dt in ("f32", "bf16"):
+        bf16 = dt == "bf16"
+        gs = make_grads("like", 61, world, L, bf16)
+        w0, v0 = synth.w_like(61, L), synth.w_like(62, L)
+        w_exp, v_exp = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, 0.001)
+        g = to_dev(gs[rank], bf16, dev)
+        w, v = to_dev(w0, dev=dev), to_dev(v0, dev=dev)
+        gdraa.gdraa_register(w)
+        gdraa.gdraa_register(g)
+        done = torch.cuda.Event()
+        for first, count in BUCKETS:
+            done.record(torch.cuda.current_stream())     # "the bucket's gradient is ready"
+            side.wait_event(done)
+            gdraa.gdraa_sgd_step_range(w, g, v, first, count, 0.1, 0.9, 0.001, stream=side)
+        side.synchronize()
+        compare(from_dev(w), w_exp, "f32", what=f"bucketed w {dt} r{rank}")
+        vh = from_dev(v)
+        for first, count in BUCKETS:
+            off, ln = gdraa.gdraa_shard(world, rank, count)
+            a, b = first + off, first + off + ln
+            compare(vh[a:b], v_exp[a:b], "f32", what=f"bucketed v {dt} r{rank}")
+        # allreduce_mean on the same buckets (both the LL and the two-shot sizes)
+        buf = to_dev(gs[rank], bf16, dev)
+        gdraa.gdraa_register(buf)
+        for first, count in BUCKETS:
+            gdraa.gdraa_allreduce_mean_range(buf, first, count, stream=side)
+        side.synchronize()
+        compare(from_dev(buf), oracle.allreduce_mean(gs), dt, what=f"bucketed mean {dt}")
+        for t in (w, g, buf):
+            gdraa.gdraa_deregister(t)
+    gdraa.gdraa_finalize()
+    with open(os.path.join(out_dir, f"bucket{rank}.ok"), "w") as f:
+        f.write("ok")
+
+
+def test_multiprocess_bucketed_ranges(tmp_path):
+    from paper_1802_02326_b200 import jobserver
+    world = min(torch.cuda.device_count(), 8)
+    sock = str(tmp_path / "js.sock")
+    js = jobserver.start(world, sock)
+    try:
+        mp.start_processes(_bucket_worker, args=(world, sock, str(tmp_path)), nprocs=world,
+                           join=True, start_method="spawn")
+    finally:
+        js.communicate(timeout=120)
+    assert all((tmp_path / f"bucket{r}.ok").exists() for r in range(world))
+
+
 def _ls_worker(rank, world, sock, out_dir):
     """NEXT-4 over real processes: each rank computes its own b-sample least-squares
     gradient and steps through gdraa_sgd_step; rank 0 checks the serial trajectory."""
