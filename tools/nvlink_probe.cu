@@ -380,6 +380,36 @@ int main(int argc, char **argv) {
             });
         }
     }
+    // How many SMs does each mechanism need?  (bidirectional, fixed per-CTA shapes)
+    {
+        constexpr int ST = 8, CH = 16384;
+        auto kp = tma_pull<ST, CH, true>;
+        auto ks = tma_push<ST, CH>;
+        for (int d = 0; d < 2; ++d) {
+            CK(cudaSetDevice(d));
+            CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, ST * CH));
+            CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, ST * CH));
+        }
+        for (int grid : {8, 16, 32, 64, 96, 148}) {
+            char name[64];
+            std::snprintf(name, sizeof name, "ctas%03d_pull_u4_1024thr", grid);
+            run_bidir(name, bytes, [&](int d, cudaStream_t s) {
+                copy_kernel<4><<<grid, 1024, 0, s>>>((const uint4 *)p.buf[1 - d][0], (uint4 *)p.buf[d][1], n16);
+            });
+            std::snprintf(name, sizeof name, "ctas%03d_push_u4_1024thr", grid);
+            run_bidir(name, bytes, [&](int d, cudaStream_t s) {
+                copy_kernel<4><<<grid, 1024, 0, s>>>((const uint4 *)p.buf[d][0], (uint4 *)p.buf[1 - d][2], n16);
+            });
+            std::snprintf(name, sizeof name, "ctas%03d_tma_pull_st8", grid);
+            run_bidir(name, bytes, [&](int d, cudaStream_t s) {
+                kp<<<grid, 32, ST * CH, s>>>(p.buf[1 - d][0], p.buf[d][1], bytes);
+            });
+            std::snprintf(name, sizeof name, "ctas%03d_tma_push_st8", grid);
+            run_bidir(name, bytes, [&](int d, cudaStream_t s) {
+                ks<<<grid, 32, ST * CH, s>>>(p.buf[d][0], p.buf[1 - d][2], bytes);
+            });
+        }
+    }
     // cudaMemcpyPeerAsync reference
     run_bidir("memcpy_peer", bytes, [&](int d, cudaStream_t s) {
         CK(cudaMemcpyPeerAsync(p.buf[1 - d][2], 1 - d, p.buf[d][0], d, bytes, s));
