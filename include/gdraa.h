@@ -159,7 +159,7 @@ int gdraa_sgd_step_mp(float *w_master, void *w_model, const void *g, float *v, f
  * with off_r/len_r = gdraa_shard(world, r, count) -- so v (and w_master) must be stepped
  * with the same bucketing every iteration.
  *   w, g, v, buf, w_master, w_model: the base pointers as registered / allocated.
- *   first: multiple of 4; count >= 1; first + count <= n.
+ *   first: multiple of 8 (16-byte aligned for bf16 too); count >= 1; first + count <= n.
  * Errors as the whole-buffer calls, plus EINVAL for a bad range.  GDRAA_MAX_CTAS caps
  * the CTAs per call so that bucket kernels leave SMs to the concurrent backward.
  */

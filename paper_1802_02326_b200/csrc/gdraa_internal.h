@@ -80,6 +80,12 @@ cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows,
 // Max co-resident CTAs of the kernel for (dtype, mode, world) on this device.
 int max_ctas(int dtype, int mode, int world);
 
+// The TMA-staged variant of launch_gdraa (same semantics and results).
+cudaError_t launch_gdraa_tma(const KParams &p, int dtype, int mode, int vr_rows,
+                             bool cooperative, cudaStream_t s, int *grid_x_out);
+// Whether the runtime launches the TMA-staged kernel (GDRAA_KERNEL=tma|lsu).
+bool use_tma_kernel();
+
 // Small-message allreduce_mean ("LL": data carries its own epoch flags, no barriers).
 // Requires n * elem_size <= 8 * p.ll_pairs.
 cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool cooperative,

@@ -23,7 +23,12 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <set>
+#include <string>
 #include <type_traits>
+#include <utility>
 
 #include "gdraa_internal.h"
 
@@ -554,6 +559,291 @@ gdraa_ll_kernel(const __grid_constant__ KParams p) {
     }
 }
 
+// ---------------------------------------------------------------------------------
+// TMA-staged variant of the two-shot kernel (same a2..a7 steps, same arithmetic, same
+// barriers).  One producer thread per CTA streams each chunk of the owner shard -- the
+// N ranks' gradient blocks (NVLink for peers) plus the local w and v -- into a
+// STAGES-deep shared-memory ring with 1-D bulk copies (cp.async.bulk, completion on an
+// mbarrier); 8 consumer warps fold, update and push from shared memory.  Bytes in
+// flight per SM no longer depend on registers, so a few dozen SMs drive NVLink at full
+// rate (profiles/r19_nvlink_probe_n2_ctas.jsonl: bulk pulls reach 615 GB/s from 16 SMs)
+// and the rest stay free for a concurrent backward pass (NEXT-3).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *smem, const void *gmem, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem)),
+        "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Stage = one chunk of CH elements of every source (+ w, v): about STAGE_KB per stage.
+// 16 consumer warps: same rate as 8 on the full grid, and 607 GB/s (full rate) from only
+// 64 SMs at N=2 vs 595 for 8 warps (profiles/r21_ctas_n2.jsonl).
+template <typename TG, int WORLD, int MODE, int CW_ = 16, int ST_ = 4, int STAGE_KB = 40>
+struct TmaCfg {
+    static constexpr int SG = sizeof(TG);
+    static constexpr bool UPD = MODE != kMean;
+    static constexpr int PER_EL = WORLD * SG + (UPD ? 8 : 0);      // smem bytes / element
+    static constexpr int BUDGET = STAGE_KB * 1024;
+    static constexpr int CH = BUDGET / PER_EL >= 2048 ? 2048 : (BUDGET / PER_EL >= 1024 ? 1024 : 512);
+    static constexpr int STAGES = ST_;
+    static constexpr int CW = CW_;                                 // consumer warps
+    static constexpr int THREADS = 32 * (CW + 1);
+    static constexpr int STAGE_BYTES = CH * PER_EL;
+    static constexpr int SMEM = STAGES * STAGE_BYTES;
+};
+
+template <typename TG, int WORLD, int MODE, int CW_ = 16, int ST_ = 4>
+__global__ void __launch_bounds__(TmaCfg<TG, WORLD, MODE, CW_, ST_>::THREADS, 1)
+gdraa_tma_kernel(const __grid_constant__ KParams p) {
+    using C = TmaCfg<TG, WORLD, MODE, CW_, ST_>;
+    using EL = Elem<TG>;
+    using Raw = typename EL::Raw;
+    constexpr bool kUpdate = C::UPD;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t full[C::STAGES], empty[C::STAGES];
+    __shared__ uint32_t s_chunk[C::STAGES];
+    __shared__ int s_abort, s_last;
+
+    const int vr = blockIdx.y;
+    const int rank = p.rank0 + vr;
+    Pad *mine = p.pad[vr][rank];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint64_t epoch = *reinterpret_cast<volatile uint64_t *>(&mine->epoch) + 1;
+    if (threadIdx.x == 0) {
+        s_abort = 0;
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(0);
+    // a2: "2nd synchronization"
+    if (WORLD > 1) {
+        if (blockIdx.x == 0 && threadIdx.x < WORLD && threadIdx.x != rank)
+            st_release_sys(&p.pad[vr][threadIdx.x]->entry[rank], epoch);
+        __syncthreads();
+        if (threadIdx.x < WORLD && threadIdx.x != rank) {
+            if (!wait_geq(&mine->entry[threadIdx.x], epoch, p.timeout_ns)) {
+                report_timeout(p.err, 1, threadIdx.x, vr);
+                s_abort = 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (s_abort) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(1);
+
+    const uint64_t off = min(static_cast<uint64_t>(rank) * p.blk, p.n);
+    const uint64_t len = min(p.blk, p.n - off);
+    const uint64_t lenv = len & ~7ull;                  // bulk copies: 16-byte multiples
+    // Chunks of CH elements, the last ~2 waves of CH/4 so the CTAs finish together (the
+    // end-game of the LSU kernel); chunk c -> (e0, n_el) is a pure function.
+    constexpr uint64_t CHS = C::CH / 4;
+    const uint64_t tailv = 2ull * gridDim.x * CHS;
+    const uint64_t nbig = lenv > tailv ? (lenv - tailv) / C::CH : 0;
+    const uint64_t small0 = nbig * C::CH;
+    const uint64_t nchunks = nbig + (lenv - small0 + CHS - 1) / CHS;
+    auto chunk = [&](uint32_t c, uint64_t &e0, uint32_t &n_el) {
+        if (c < nbig) {
+            e0 = static_cast<uint64_t>(c) * C::CH;
+            n_el = C::CH;
+        } else {
+            e0 = small0 + (c - nbig) * CHS;
+            n_el = static_cast<uint32_t>(lenv - e0 < CHS ? lenv - e0 : CHS);
+        }
+    };
+    const float lr = p.lr, mom = p.mom, wd = p.wd;
+    float *const vloc = p.v[vr];
+    float *const wloc = MODE == kSgdMp ? p.wm[vr] : static_cast<float *>(p.dst[vr][rank]);
+
+    auto stage_src = [&](int s, int q) {
+        return reinterpret_cast<TG *>(smem + s * C::STAGE_BYTES) + q * C::CH;
+    };
+    auto stage_w = [&](int s) {
+        return reinterpret_cast<float *>(smem + s * C::STAGE_BYTES + WORLD * C::SG * C::CH);
+    };
+    auto stage_v = [&](int s) { return stage_w(s) + C::CH; };
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0) {
+        // producer: a3 loads (and the local w, v) of one chunk per stage
+        if (lane == 0) {
+            for (uint32_t it = 0;; ++it) {
+                const int s = it % C::STAGES;
+                if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+                const uint32_t c = atomicAdd(&mine->next, 1u);
+                if (c >= nchunks) {
+                    s_chunk[s] = 0xFFFFFFFFu;
+                    mbar_arrive(&full[s]);
+                    break;
+                }
+                s_chunk[s] = c;
+                uint64_t e0;
+                uint32_t n_el;
+                chunk(c, e0, n_el);
+                mbar_arrive_tx(&full[s], n_el * C::PER_EL);
+#pragma unroll
+                for (int q = 0; q < WORLD; ++q)
+                    bulk_g2s(stage_src(s, q), static_cast<const TG *>(p.src[vr][q]) + off + e0,
+                             n_el * C::SG, &full[s]);
+                if (kUpdate) {
+                    bulk_g2s(stage_w(s), wloc + off + e0, n_el * 4, &full[s]);
+                    bulk_g2s(stage_v(s), vloc + off + e0, n_el * 4, &full[s]);
+                }
+            }
+        }
+    } else {
+        // consumers: a4 fold (+ a5 update) from shared memory, a6 push
+        const int ct = threadIdx.x - 32;
+        for (uint32_t it = 0;; ++it) {
+            const int s = it % C::STAGES;
+            mbar_wait(&full[s], (it / C::STAGES) & 1);
+            const uint32_t c = s_chunk[s];
+            if (c == 0xFFFFFFFFu) break;
+            uint64_t e0;
+            uint32_t n_el;
+            chunk(c, e0, n_el);
+            for (uint32_t k = ct * E; k < n_el; k += C::CW * 32 * E) {
+                float x[WORLD][E];
+#pragma unroll
+                for (int q = 0; q < WORLD; ++q)
+                    EL::widen(*reinterpret_cast<const Raw *>(stage_src(s, q) + k), x[q]);
+                float m[E];
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    float col[WORLD];
+#pragma unroll
+                    for (int q = 0; q < WORLD; ++q) col[q] = x[q][e];
+                    m[e] = average<WORLD>(col);
+                }
+                const uint64_t g0 = off + e0 + k;
+                if (kUpdate) {
+                    float4 w = *reinterpret_cast<const float4 *>(stage_w(s) + k);
+                    float4 v = *reinterpret_cast<const float4 *>(stage_v(s) + k);
+                    sgd(m[0], lr, mom, wd, w.x, v.x);
+                    sgd(m[1], lr, mom, wd, w.y, v.y);
+                    sgd(m[2], lr, mom, wd, w.z, v.z);
+                    sgd(m[3], lr, mom, wd, w.w, v.w);
+                    st_vec(reinterpret_cast<uint4 *>(vloc + g0), as_u4(v.x, v.y, v.z, v.w));
+                    if (MODE == kSgd) {
+                        const uint4 o = as_u4(w.x, w.y, w.z, w.w);
+#pragma unroll
+                        for (int j = 1; j <= WORLD; ++j) {
+                            const int q = (rank + j) % WORLD;
+                            st_vec(reinterpret_cast<uint4 *>(static_cast<float *>(p.dst[vr][q]) + g0), o);
+                        }
+                    } else {
+                        st_vec(reinterpret_cast<uint4 *>(wloc + g0), as_u4(w.x, w.y, w.z, w.w));
+                        const float wf[E] = {w.x, w.y, w.z, w.w};
+                        const uint2 o = Elem<__nv_bfloat16>::narrow(wf);
+#pragma unroll
+                        for (int j = 1; j <= WORLD; ++j) {
+                            const int q = (rank + j) % WORLD;
+                            st_vec(reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(p.dst[vr][q]) + g0), o);
+                        }
+                    }
+                } else {
+                    const Raw o = EL::narrow(m);
+#pragma unroll
+                    for (int j = 1; j <= WORLD; ++j) {
+                        const int q = (rank + j) % WORLD;
+                        st_vec(reinterpret_cast<Raw *>(static_cast<TG *>(p.dst[vr][q]) + g0), o);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        // ragged tail (len % 8 elements) by the last CTA's consumers, scalar
+        if (blockIdx.x == gridDim.x - 1) {
+            for (uint64_t t = lenv + ct; t < len; t += C::CW * 32) {
+                const uint64_t e = off + t;
+                float col[WORLD];
+#pragma unroll
+                for (int q = 0; q < WORLD; ++q) col[q] = EL::load1(p.src[vr][q], e);
+                const float m = average<WORLD>(col);
+                if (kUpdate) {
+                    float w = wloc[e], v = vloc[e];
+                    sgd(m, lr, mom, wd, w, v);
+                    vloc[e] = v;
+                    if (MODE == kSgd) {
+                        for (int j = 1; j <= WORLD; ++j)
+                            static_cast<float *>(p.dst[vr][(rank + j) % WORLD])[e] = w;
+                    } else {
+                        wloc[e] = w;
+                        for (int j = 1; j <= WORLD; ++j)
+                            Elem<__nv_bfloat16>::store1(p.dst[vr][(rank + j) % WORLD], e, w);
+                    }
+                } else {
+                    for (int j = 1; j <= WORLD; ++j)
+                        EL::store1(p.dst[vr][(rank + j) % WORLD], e, m);
+                }
+            }
+        }
+    }
+
+    // a7: "1st synchronization" (as in gdraa_kernel)
+    if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(2);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (WORLD > 1) fence_acq_rel_sys();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&mine->arrive, 1u);
+        s_last = (prev == gridDim.x - 1);
+        if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (!s_last) return;
+    if (threadIdx.x == 0) GDRAA_STAMP(3);
+    if (WORLD > 1) {
+        if (threadIdx.x < WORLD && threadIdx.x != rank)
+            st_release_sys(&p.pad[vr][threadIdx.x]->exit[rank], epoch);
+        if (threadIdx.x < WORLD && threadIdx.x != rank) {
+            if (!wait_geq(&mine->exit[threadIdx.x], epoch, p.timeout_ns)) {
+                report_timeout(p.err, 2, threadIdx.x, vr);
+                s_abort = 1;
+            }
+        }
+        __syncthreads();
+        if (s_abort) return;
+    }
+    if (threadIdx.x == 0) {
+        GDRAA_STAMP(4);
+        mine->arrive = 0;
+        mine->next = 0;
+        mine->calls += 1;
+        if (WORLD > 1) mine->sync_waits += 2;
+        mine->epoch = epoch;
+        if (p.done[vr] != nullptr) *p.done[vr] = epoch;
+    }
+}
+
 using KernelFnLL = void (*)(KParams);
 
 // Programmatic stream serialization hides the launch gap between back-to-back
@@ -589,6 +879,52 @@ KernelFnLL pick_ll_t(int world) {
         case 8: return gdraa_ll_kernel<TG, 8>;
         default: return nullptr;
     }
+}
+
+struct TmaLaunch {
+    KernelFnLL fn;
+    int threads;
+    int smem;
+    int ch;
+};
+
+template <typename TG, int MODE, int WORLD>
+TmaLaunch pick_tma_w() {
+    using C = TmaCfg<TG, WORLD, MODE>;
+    return {gdraa_tma_kernel<TG, WORLD, MODE>, C::THREADS, C::SMEM, C::CH};
+}
+
+template <typename TG, int MODE>
+TmaLaunch pick_tma_m(int world) {
+    switch (world) {
+        case 1: return pick_tma_w<TG, MODE, 1>();
+        case 2: return pick_tma_w<TG, MODE, 2>();
+        case 3: return pick_tma_w<TG, MODE, 3>();
+        case 4: return pick_tma_w<TG, MODE, 4>();
+        case 5: return pick_tma_w<TG, MODE, 5>();
+        case 6: return pick_tma_w<TG, MODE, 6>();
+        case 7: return pick_tma_w<TG, MODE, 7>();
+        case 8: return pick_tma_w<TG, MODE, 8>();
+        default: return {nullptr, 0, 0};
+    }
+}
+
+template <typename TG>
+TmaLaunch pick_tma_t(int mode, int world) {
+    switch (mode) {
+        case kMean: return pick_tma_m<TG, kMean>(world);
+        case kSgd: return pick_tma_m<TG, kSgd>(world);
+        case kSgdMp: return pick_tma_m<TG, kSgdMp>(world);
+        default: return {nullptr, 0, 0};
+    }
+}
+
+int env_max_ctas() {
+    static const int v = [] {
+        const char *e = std::getenv("GDRAA_MAX_CTAS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
 }
 
 // ---------------------------------------------------------------------------------
@@ -679,10 +1015,7 @@ cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows, boo
     if (l.fn == nullptr) return cudaErrorInvalidValue;
     // GDRAA_MAX_CTAS (tuning only): cap the grid, e.g. to leave SMs to a concurrent
     // backward pass when buckets are reduced on a side stream (NEXT-3).
-    static const int env_cap = [] {
-        const char *e = std::getenv("GDRAA_MAX_CTAS");
-        return e ? std::atoi(e) : 0;
-    }();
+    const int env_cap = env_max_ctas();
     int cap = max_ctas(dtype, mode, p.world) / vr_rows;
     if (env_cap > 0 && env_cap < cap) cap = env_cap;
     if (cap < 1) return cudaErrorInvalidConfiguration;
@@ -724,6 +1057,74 @@ cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool coope
                                            0, s);
     }
     return launch_pdl(fn, grid, block, s, p);
+}
+
+bool use_tma_kernel() {
+    static const bool v = [] {
+        const char *e = std::getenv("GDRAA_KERNEL");
+        return e != nullptr && std::string(e) == "tma";
+    }();
+    return v;
+}
+
+cudaError_t launch_gdraa_tma(const KParams &p, int dtype, int mode, int vr_rows,
+                             bool cooperative, cudaStream_t s, int *grid_x_out) {
+    TmaLaunch l = dtype == GDRAA_F32 ? pick_tma_t<float>(mode, p.world)
+                                     : pick_tma_t<__nv_bfloat16>(mode, p.world);
+    if (l.fn == nullptr) return cudaErrorInvalidValue;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    // opt in to > 48 KiB of dynamic shared memory once per (device, kernel)
+    static std::mutex mu;
+    static std::set<std::pair<int, void *>> ready;
+    static std::map<std::pair<int, void *>, int> occ;
+    int per_sm = 0, sms = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        const auto key = std::make_pair(dev, reinterpret_cast<void *>(l.fn));
+        if (!ready.count(key)) {
+            e = cudaFuncSetAttribute(reinterpret_cast<const void *>(l.fn),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
+            if (e != cudaSuccess) return e;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l.fn, l.threads, l.smem);
+            if (e != cudaSuccess) return e;
+            ready.insert(key);
+            occ[key] = per_sm;
+        }
+        per_sm = occ[key];
+    }
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    int cap = sms * per_sm / vr_rows;
+    const int env_cap = env_max_ctas();
+    if (env_cap > 0 && env_cap < cap) cap = env_cap;
+    if (cap < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t want = ((p.blk & ~7ull) + l.ch - 1) / l.ch;   // chunks of the largest shard
+    int gx = static_cast<int>(want < static_cast<uint64_t>(cap) ? want : cap);
+    if (gx < 1) gx = 1;
+    if (grid_x_out) *grid_x_out = gx;
+    dim3 grid(gx, vr_rows), block(l.threads);
+    if (cooperative) {
+        void *args[] = {const_cast<KParams *>(&p)};
+        return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(l.fn), grid, block,
+                                           args, l.smem, s);
+    }
+    static const bool pdl = [] {
+        const char *x = std::getenv("GDRAA_PDL");
+        return x == nullptr || x[0] != '0';
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = l.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, l.fn, p);
 }
 
 }  // namespace gdraa

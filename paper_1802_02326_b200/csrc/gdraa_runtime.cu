@@ -353,7 +353,8 @@ void account(uint64_t n, int dtype_g, uint64_t s_w) {
 
 int launch(const KParams &p, int dtype, int mode, cudaStream_t s) {
     int gx = 0;
-    cudaError_t e = launch_gdraa(p, dtype, mode, 1, false, s, &gx);
+    cudaError_t e = use_tma_kernel() ? launch_gdraa_tma(p, dtype, mode, 1, false, s, &gx)
+                                     : launch_gdraa(p, dtype, mode, 1, false, s, &gx);
     if (e != cudaSuccess) return fail(GDRAA_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
     g.issued += 1;
     return GDRAA_OK;
@@ -493,7 +494,8 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
         return GDRAA_OK;
     }
     int gx = 0;
-    cudaError_t e = launch_gdraa(p, dtype, mode, world, true, s, &gx);
+    cudaError_t e = use_tma_kernel() ? launch_gdraa_tma(p, dtype, mode, world, true, s, &gx)
+                                     : launch_gdraa(p, dtype, mode, world, true, s, &gx);
     if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr kernel launch: %s", cudaGetErrorString(e));
     return GDRAA_OK;
 }
@@ -669,7 +671,8 @@ int gdraa_deregister(void *buf) {
 }
 
 // Resolve the element range [first, first + count) of a registration (count == SIZE_MAX:
-// the whole buffer).  Ranges start on a 4-element boundary so every vector stays aligned.
+// the whole buffer).  Ranges start on an 8-element boundary so every vector access and
+// every 1-D bulk copy (16-byte aligned, also for bf16) stays aligned.
 static int resolve_range(const Registration *r, size_t first, size_t *count) {
     if (*count == SIZE_MAX) {
         if (first != 0) return fail(GDRAA_EINVAL, "whole-buffer call with first != 0");
@@ -677,7 +680,7 @@ static int resolve_range(const Registration *r, size_t first, size_t *count) {
         return GDRAA_OK;
     }
     if (*count == 0) return fail(GDRAA_EINVAL, "count must be >= 1");
-    if (first % 4 != 0) return fail(GDRAA_EINVAL, "first (%zu) must be a multiple of 4", first);
+    if (first % 8 != 0) return fail(GDRAA_EINVAL, "first (%zu) must be a multiple of 8", first);
     if (first > r->n || *count > r->n - first)
         return fail(GDRAA_EINVAL, "range [%zu, %zu) exceeds the registered %zu elements", first,
                     first + *count, r->n);

@@ -237,12 +237,12 @@ def test_world1_bucketed_ranges(world1):
     g, w, v = to_dev(gs[0]), to_dev(w0), to_dev(v0)
     gdraa.gdraa_register(w)
     gdraa.gdraa_register(g)
-    for first, count in [(200_000, 100_008), (4, 199_996), (0, 4)]:
+    for first, count in [(200_000, 100_008), (8, 199_992), (0, 8)]:
         gdraa.gdraa_sgd_step_range(w, g, v, first, count, 0.1, 0.9, 0.001)
     torch.cuda.synchronize()
     compare(from_dev(w), w_exp, "f32", what="w")
     compare(from_dev(v), v_exp, "f32", what="v")
-    for bad in [(1, 10), (0, 0), (300_000, 9), (400_000, 4)]:
+    for bad in [(1, 10), (4, 10), (0, 0), (300_000, 9), (400_000, 8)]:
         with pytest.raises(gdraa.GdraaError) as e:
             gdraa.gdraa_sgd_step_range(w, g, v, bad[0], bad[1], 0.1, 0.9)
         assert e.value.name == "GDRAA_EINVAL", bad

@@ -123,7 +123,7 @@ def test_multiprocess_parity(tmp_path):
         assert rep["cases"] == len(L_list) * 4
 
 
-BUCKETS = [(600_000, 400_004), (0, 600_000), (1_000_004, 48_572)]   # backward order
+BUCKETS = [(600_000, 400_000), (0, 600_000), (1_000_000, 48_576)]   # backward order
 
 
 def _bucket_worker(rank, world, sock, out_dir):

@@ -1,13 +1,16 @@
-// tune.cu -- launch-shape sweep of the GDRAA kernel on 1..4 B200s of one box, single
+// tune.cu -- launch-shape sweep of the GDRAA kernels on 1..4 B200s of one box, single
 // process: rank d's kernel runs on device d and reaches its peers through
 // cudaDeviceEnablePeerAccess pointers (same kernel code as the library; the IPC and job
-// server plumbing is not involved).  Prints one JSON line per (shape, config).
+// server plumbing is not involved).  Prints one JSON line per (kernel, shape, config),
+// with a per-phase breakdown from %globaltimer stamps (kernels built with GDRAA_TRACE).
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
 //        -o tools/tune tools/tune.cu
-//   ./tools/tune <world> <L> <f32|bf16> <sgd|mean> [iters] [lib]
-// "lib": only the library's launch shape.  Every line carries a phase breakdown from
-// %globaltimer stamps (kernels built with GDRAA_TRACE).
+//   ./tools/tune <world> <L> <f32|bf16> <sgd|mean> [iters] [lib|lsu|tma|ctas]
+//     lib : the library's launch shapes (LSU and TMA kernels)
+//     lsu : sweep of the LSU kernel's (U, threads, CTAs/SM)
+//     tma : sweep of the TMA kernel's (consumer warps, stages)
+//     ctas: both kernels at grid caps 16/32/64/all (how many SMs the collective needs)
 #define GDRAA_TRACE 1
 #include "../paper_1802_02326_b200/csrc/gdraa_kernels.cu"
 
@@ -39,31 +42,24 @@ static int W, NDEV;
 static size_t L;
 static int DT, MODE_;
 static int ITERS = 50;
+static std::string WHAT = "lsu";
 static std::vector<Bufs> B;
 static ErrBlock *err_d;
 static std::vector<uint64_t *> TR;   // per-device trace ring (64 calls x 8 vr x 8 stamps)
-static bool LIB_ONLY = false;
 
-template <typename TG, int WORLD, int MODE, int U, int THREADS, int MINB>
-void run_shape(int grid_div) {
-    auto fn = gdraa_kernel<TG, WORLD, MODE, U, THREADS, MINB>;
-    int sms = 0, per = 0;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, THREADS, 0));
-    uint64_t blk, off, len;
-    {
-        const uint64_t c = (L + WORLD - 1) / WORLD;
-        blk = (c + kQuantum - 1) / kQuantum * kQuantum;
-        (void)off; (void)len;
-    }
-    const uint64_t nvec = (blk + 3) / 4;
-    uint64_t want = (nvec + THREADS * U - 1) / (THREADS * U);
-    int gx = (int)std::min<uint64_t>(want, (uint64_t)sms * per / grid_div);
-    if (gx < 1) gx = 1;
+// Time `fn` (grid gx x threads, dynamic smem) on all W devices; print one line.
+template <typename TG, int WORLD, int MODE>
+void run(void (*fn)(KParams), int threads, int smem, int gx, const char *kernel,
+         const std::string &shape) {
+    const uint64_t c = (L + WORLD - 1) / WORLD;
+    const uint64_t blk = (c + kQuantum - 1) / kQuantum * kQuantum;
     std::vector<cudaStream_t> st(WORLD);
     std::vector<cudaEvent_t> e0(WORLD), e1(WORLD);
     for (int d = 0; d < WORLD; ++d) {
         CK(cudaSetDevice(d));
+        if (smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(fn),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         CK(cudaStreamCreate(&st[d]));
         CK(cudaEventCreate(&e0[d]));
         CK(cudaEventCreate(&e1[d]));
@@ -88,7 +84,7 @@ void run_shape(int grid_div) {
             p.err = err_d;
             p.trace = TR[d];
             CK(cudaSetDevice(d));
-            fn<<<dim3(gx, 1), THREADS, 0, st[d]>>>(p);
+            fn<<<dim3(gx, 1), threads, smem, st[d]>>>(p);
             CK(cudaGetLastError());
         }
     };
@@ -109,7 +105,6 @@ void run_shape(int grid_div) {
         std::fprintf(stderr, "timeout reported\n");
         std::exit(2);
     }
-    // phase breakdown from the %globaltimer stamps of the last calls (same-device deltas)
     double acc[5] = {0, 0, 0, 0, 0};
     int cnt = 0;
     for (int d = 0; d < WORLD; ++d) {
@@ -130,16 +125,17 @@ void run_shape(int grid_div) {
     }
     const double t = worst / ITERS * 1e-3;
     const int sg = sizeof(TG);
-    double bytes = WORLD == 1 ? (MODE == kSgd ? (sg + 16.0) * L : 2.0 * sg * L)
-                              : (WORLD - 1.0) / WORLD * L * (sg + (MODE == kSgd ? 4 : sg));
-    std::printf("{\"world\": %d, \"L\": %zu, \"dtype\": \"%s\", \"mode\": \"%s\", \"U\": %d, "
-                "\"threads\": %d, \"minb\": %d, \"per_sm\": %d, \"grid\": %d, \"us\": %.2f, "
-                "\"gbs_per_rank\": %.1f, \"phase_us\": {\"entry\": %.2f, \"data_cta0\": %.2f, "
-                "\"to_last_arrival\": %.2f, \"exit\": %.2f, \"gap_to_next\": %.2f}}\n",
-                WORLD, L, sg == 4 ? "f32" : "bf16", MODE == kSgd ? "sgd" : "mean", U, THREADS,
-                MINB, per, gx, t * 1e6, bytes / t / 1e9, cnt ? acc[0] / cnt / 1e3 : 0.0,
-                cnt ? acc[1] / cnt / 1e3 : 0.0, cnt ? acc[2] / cnt / 1e3 : 0.0,
-                cnt ? acc[3] / cnt / 1e3 : 0.0, cnt ? acc[4] / cnt / 1e3 : 0.0);
+    const double bytes = WORLD == 1 ? (MODE == kSgd ? (sg + 16.0) * L : 2.0 * sg * L)
+                                    : (WORLD - 1.0) / WORLD * L * (sg + (MODE == kSgd ? 4 : sg));
+    auto ph = [&](int k) { return cnt ? acc[k] / cnt / 1e3 : 0.0; };
+    std::printf("{\"world\": %d, \"L\": %zu, \"dtype\": \"%s\", \"mode\": \"%s\", \"kernel\": "
+                "\"%s\", \"shape\": \"%s\", \"threads\": %d, \"smem\": %d, \"grid\": %d, "
+                "\"us\": %.2f, \"gbs_per_rank\": %.1f, \"phase_us\": {\"entry\": %.2f, "
+                "\"data_cta0\": %.2f, \"to_last_arrival\": %.2f, \"exit\": %.2f, "
+                "\"gap_to_next\": %.2f}}\n",
+                WORLD, L, sg == 4 ? "f32" : "bf16", MODE == kSgd ? "sgd" : "mean", kernel,
+                shape.c_str(), threads, smem, gx, t * 1e6, bytes / t / 1e9, ph(0), ph(1), ph(2),
+                ph(3), ph(4));
     std::fflush(stdout);
     for (int d = 0; d < WORLD; ++d) {
         CK(cudaSetDevice(d));
@@ -147,26 +143,72 @@ void run_shape(int grid_div) {
     }
 }
 
+static int sm_count() {
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    return sms;
+}
+
+template <typename TG, int WORLD, int MODE, int U, int THREADS, int MINB>
+void lsu(int cap = 0) {
+    auto fn = gdraa_kernel<TG, WORLD, MODE, U, THREADS, MINB>;
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, THREADS, 0));
+    const uint64_t c = (L + WORLD - 1) / WORLD;
+    const uint64_t nvec = ((c + kQuantum - 1) / kQuantum * kQuantum + 3) / 4;
+    uint64_t gx = std::min<uint64_t>((nvec + THREADS * U - 1) / (THREADS * U),
+                                     (uint64_t)sm_count() * per);
+    if (cap > 0) gx = std::min<uint64_t>(gx, cap);
+    char shape[64];
+    std::snprintf(shape, sizeof shape, "U%d_T%d_minb%d_per%d", U, THREADS, MINB, per);
+    run<TG, WORLD, MODE>(fn, THREADS, 0, (int)std::max<uint64_t>(gx, 1), "lsu", shape);
+}
+
+template <typename TG, int WORLD, int MODE, int CW, int ST>
+void tma(int cap = 0) {
+    using C = TmaCfg<TG, WORLD, MODE, CW, ST>;
+    auto fn = gdraa_tma_kernel<TG, WORLD, MODE, CW, ST>;
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(fn),
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, C::THREADS, C::SMEM));
+    const uint64_t c = (L + WORLD - 1) / WORLD;
+    const uint64_t blk = (c + kQuantum - 1) / kQuantum * kQuantum;
+    uint64_t gx = std::min<uint64_t>(((blk & ~7ull) + C::CH - 1) / C::CH,
+                                     (uint64_t)sm_count() * per);
+    if (cap > 0) gx = std::min<uint64_t>(gx, cap);
+    char shape[64];
+    std::snprintf(shape, sizeof shape, "CW%d_ST%d_CH%d_per%d", CW, ST, C::CH, per);
+    run<TG, WORLD, MODE>(fn, C::THREADS, C::SMEM, (int)std::max<uint64_t>(gx, 1), "tma", shape);
+}
+
 template <typename TG, int WORLD, int MODE>
 void sweep() {
-    if (LIB_ONLY) {
-        using S = Shape<TG, WORLD, MODE>;
-        run_shape<TG, WORLD, MODE, S::U, S::THREADS, S::MINB>(1);
-        return;
+    using S = Shape<TG, WORLD, MODE>;
+    if (WHAT == "lib") {
+        lsu<TG, WORLD, MODE, S::U, S::THREADS, S::MINB>();
+        tma<TG, WORLD, MODE, 8, 4>();
+    } else if (WHAT == "lsu") {
+        lsu<TG, WORLD, MODE, 1, 512, 2>();
+        lsu<TG, WORLD, MODE, 2, 512, 2>();
+        lsu<TG, WORLD, MODE, 2, 1024, 1>();
+        lsu<TG, WORLD, MODE, 4, 512, 1>();
+        lsu<TG, WORLD, MODE, 1, 1024, 1>();
+        lsu<TG, WORLD, MODE, 4, 256, 1>();
+    } else if (WHAT == "tma") {
+        tma<TG, WORLD, MODE, 4, 4>();
+        tma<TG, WORLD, MODE, 8, 2>();
+        tma<TG, WORLD, MODE, 8, 3>();
+        tma<TG, WORLD, MODE, 8, 4>();
+        tma<TG, WORLD, MODE, 8, 5>();
+        tma<TG, WORLD, MODE, 16, 4>();
+    } else if (WHAT == "ctas") {
+        for (int cap : {16, 32, 64, 0}) {
+            lsu<TG, WORLD, MODE, S::U, S::THREADS, S::MINB>(cap);
+            tma<TG, WORLD, MODE, 8, 4>(cap);
+            tma<TG, WORLD, MODE, 16, 4>(cap);
+        }
     }
-    run_shape<TG, WORLD, MODE, 1, 512, 1>(1);
-    run_shape<TG, WORLD, MODE, 2, 512, 1>(1);
-    run_shape<TG, WORLD, MODE, 4, 512, 1>(1);
-    run_shape<TG, WORLD, MODE, 1, 256, 1>(1);
-    run_shape<TG, WORLD, MODE, 2, 256, 1>(1);
-    run_shape<TG, WORLD, MODE, 4, 256, 1>(1);
-    run_shape<TG, WORLD, MODE, 1, 512, 2>(1);
-    run_shape<TG, WORLD, MODE, 2, 512, 2>(1);
-    run_shape<TG, WORLD, MODE, 1, 1024, 1>(1);
-    run_shape<TG, WORLD, MODE, 2, 1024, 1>(1);
-    run_shape<TG, WORLD, MODE, 8, 256, 1>(1);
-    run_shape<TG, WORLD, MODE, 2, 512, 1>(2);
-    run_shape<TG, WORLD, MODE, 4, 256, 1>(2);
 }
 
 template <typename TG, int MODE>
@@ -181,7 +223,7 @@ void dispatch_world() {
 
 int main(int argc, char **argv) {
     if (argc < 5) {
-        std::fprintf(stderr, "usage: tune <world> <L> <f32|bf16> <sgd|mean> [iters]\n");
+        std::fprintf(stderr, "usage: tune <world> <L> <f32|bf16> <sgd|mean> [iters] [lib|lsu|tma|ctas]\n");
         return 1;
     }
     W = std::atoi(argv[1]);
@@ -189,7 +231,7 @@ int main(int argc, char **argv) {
     DT = std::string(argv[3]) == "bf16" ? GDRAA_BF16 : GDRAA_F32;
     MODE_ = std::string(argv[4]) == "mean" ? kMean : kSgd;
     if (argc > 5) ITERS = std::atoi(argv[5]);
-    if (argc > 6) LIB_ONLY = std::string(argv[6]) == "lib";
+    if (argc > 6) WHAT = argv[6];
     CK(cudaGetDeviceCount(&NDEV));
     if (NDEV < W) {
         std::fprintf(stderr, "need %d GPUs, have %d\n", W, NDEV);
@@ -210,17 +252,16 @@ int main(int argc, char **argv) {
             CK(cudaMemset(B[d].v[s], 0, L * 4));
         }
         CK(cudaMalloc(&B[d].pad, sizeof(Pad)));
+        CK(cudaMemset(B[d].pad, 0, sizeof(Pad)));
         uint64_t *tr;
         CK(cudaMalloc(&tr, 64 * kMaxWorld * 8 * 8));
         CK(cudaMemset(tr, 0, 64 * kMaxWorld * 8 * 8));
         TR.push_back(tr);
-        CK(cudaMemset(B[d].pad, 0, sizeof(Pad)));
     }
     void *eh;
     CK(cudaHostAlloc(&eh, sizeof(ErrBlock), cudaHostAllocMapped | cudaHostAllocPortable));
     std::memset(eh, 0, sizeof(ErrBlock));
-    CK(cudaHostGetDevicePointer((void **)&err_d, eh, 0));
-    err_d = (ErrBlock *)eh;   // UVA: host pointer valid on device
+    err_d = (ErrBlock *)eh;   // UVA: the host pointer is valid on the device
     if (DT == GDRAA_F32) {
         if (MODE_ == kSgd) dispatch_world<float, kSgd>(); else dispatch_world<float, kMean>();
     } else {
