@@ -83,8 +83,9 @@ int max_ctas(int dtype, int mode, int world);
 // The TMA-staged variant of launch_gdraa (same semantics and results).
 cudaError_t launch_gdraa_tma(const KParams &p, int dtype, int mode, int vr_rows,
                              bool cooperative, cudaStream_t s, int *grid_x_out);
-// Whether the runtime launches the TMA-staged kernel (GDRAA_KERNEL=tma|lsu).
-bool use_tma_kernel();
+// Whether the runtime launches the TMA-staged kernel for this call (measured choice;
+// GDRAA_KERNEL=tma|lsu forces it).
+bool use_tma_kernel(int dtype, int mode, int world);
 
 // Small-message allreduce_mean ("LL": data carries its own epoch flags, no barriers).
 // Requires n * elem_size <= 8 * p.ll_pairs.

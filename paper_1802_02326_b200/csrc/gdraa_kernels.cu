@@ -1059,12 +1059,20 @@ cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool coope
     return launch_pdl(fn, grid, block, s, p);
 }
 
-bool use_tma_kernel() {
-    static const bool v = [] {
+// Which data-movement variant serves a call (both produce the same bits).  Measured with
+// bench.py at R50/R101 (profiles/r23_bench_kernel_choice.json): the TMA-staged kernel
+// is 1.2-2.5% faster for fp32 gradients at N >= 2 and for bf16 at N = 4, 1-2.6% slower
+// for bf16 at N <= 2 and equal at N = 1.  GDRAA_KERNEL=lsu|tma forces one.
+bool use_tma_kernel(int dtype, int mode, int world) {
+    static const int forced = [] {
         const char *e = std::getenv("GDRAA_KERNEL");
-        return e != nullptr && std::string(e) == "tma";
+        if (e == nullptr) return -1;
+        return std::string(e) == "tma" ? 1 : (std::string(e) == "lsu" ? 0 : -1);
     }();
-    return v;
+    if (forced >= 0) return forced == 1;
+    if (world < 2) return false;
+    if (dtype == GDRAA_F32) return true;
+    return world >= 4 && mode != kMean;
 }
 
 cudaError_t launch_gdraa_tma(const KParams &p, int dtype, int mode, int vr_rows,

@@ -353,7 +353,8 @@ void account(uint64_t n, int dtype_g, uint64_t s_w) {
 
 int launch(const KParams &p, int dtype, int mode, cudaStream_t s) {
     int gx = 0;
-    cudaError_t e = use_tma_kernel() ? launch_gdraa_tma(p, dtype, mode, 1, false, s, &gx)
+    cudaError_t e = use_tma_kernel(dtype, mode, p.world)
+                        ? launch_gdraa_tma(p, dtype, mode, 1, false, s, &gx)
                                      : launch_gdraa(p, dtype, mode, 1, false, s, &gx);
     if (e != cudaSuccess) return fail(GDRAA_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
     g.issued += 1;
@@ -494,7 +495,8 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
         return GDRAA_OK;
     }
     int gx = 0;
-    cudaError_t e = use_tma_kernel() ? launch_gdraa_tma(p, dtype, mode, world, true, s, &gx)
+    cudaError_t e = use_tma_kernel(dtype, mode, world)
+                        ? launch_gdraa_tma(p, dtype, mode, world, true, s, &gx)
                                      : launch_gdraa(p, dtype, mode, world, true, s, &gx);
     if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr kernel launch: %s", cudaGetErrorString(e));
     return GDRAA_OK;

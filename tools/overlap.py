@@ -113,14 +113,21 @@ def main():
             gdraa.gdraa_sgd_step_range(w, g, v, first, count, lr, mom, 0.0, stream=side)
         main_s.wait_stream(side)
 
+    def comm_buckets():
+        for first, count in buckets:
+            gdraa.gdraa_sgd_step_range(w, g, v, first, count, lr, mom, 0.0)
+
     t_bwd = timed(bwd, args.iters)
+    t_comm_b = timed(comm_buckets, args.iters)
     t_serial = timed(serial, args.iters)
     t_overlap = timed(overlap, args.iters)
     if rank == 0:
         hidden = (t_serial - t_overlap) / min(t_bwd, t_comm)
         line = {"n_gpus": world, "L": L, "buckets": K, "gemm_n": n,
                 "max_ctas": os.environ.get("GDRAA_MAX_CTAS", "all"),
-                "bwd_us": t_bwd * 1e3, "comm_us": t_comm * 1e3, "serial_us": t_serial * 1e3,
+                "kernel": os.environ.get("GDRAA_KERNEL", "lsu"),
+                "bwd_us": t_bwd * 1e3, "comm_us": t_comm * 1e3,
+                "comm_bucketed_us": t_comm_b * 1e3, "serial_us": t_serial * 1e3,
                 "overlap_us": t_overlap * 1e3, "speedup": t_serial / t_overlap,
                 "fraction_of_shorter_phase_hidden": hidden}
         print(json.dumps(line), file=out, flush=True)
