@@ -110,9 +110,37 @@ __device__ __forceinline__ void report_timeout(ErrBlock *err, int phase, int pee
     do {                                                                                 \
         if (p.trace) p.trace[((epoch % 64) * kMaxWorld + vr) * 8 + (k)] = global_timer_ns(); \
     } while (0)
+// slots 5/6: earliest / latest end of any CTA's data loop (atomic min / max), reset with
+// the kernel-start stamp
+#define GDRAA_STAMP_START()                                                              \
+    do {                                                                                 \
+        if (p.trace) {                                                                   \
+            uint64_t *t_ = p.trace + ((epoch % 64) * kMaxWorld + vr) * 8;                \
+            t_[5] = ~0ull;                                                               \
+            t_[6] = 0;                                                                   \
+            t_[0] = global_timer_ns();                                                   \
+        }                                                                                \
+    } while (0)
+#define GDRAA_STAMP_DONE()                                                               \
+    do {                                                                                 \
+        __syncthreads();                                                                 \
+        if (p.trace && threadIdx.x == 0) {                                               \
+            unsigned long long *t_ = reinterpret_cast<unsigned long long *>(             \
+                p.trace + ((epoch % 64) * kMaxWorld + vr) * 8);                          \
+            const unsigned long long now_ = global_timer_ns();                           \
+            atomicMin(t_ + 5, now_);                                                     \
+            atomicMax(t_ + 6, now_);                                                     \
+        }                                                                                \
+    } while (0)
 #else
 #define GDRAA_STAMP(k) \
     do {               \
+    } while (0)
+#define GDRAA_STAMP_DONE() \
+    do {                   \
+    } while (0)
+#define GDRAA_STAMP_START() \
+    do {                    \
     } while (0)
 #endif
 
@@ -220,7 +248,7 @@ gdraa_kernel(const __grid_constant__ KParams p) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint64_t epoch = *reinterpret_cast<volatile uint64_t *>(&mine->epoch) + 1;
     if (threadIdx.x == 0) s_abort = 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP_START();
 
     // a2: "2nd synchronization" -- every peer's D(i) is final (stream-ordered after its
     // backward) before anyone reads it or writes into it.
@@ -380,6 +408,7 @@ gdraa_kernel(const __grid_constant__ KParams p) {
     // a7: "1st synchronization" -- our pushes are performed system-wide, then the last
     // CTA of this rank tells every peer and waits until every peer has done the same.
     if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(2);
+    GDRAA_STAMP_DONE();
     // Let the next kernel on the stream start launching; it waits for our completion
     // (griddepcontrol.wait above) before touching anything.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -642,7 +671,7 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP_START();
     // a2: "2nd synchronization"
     if (WORLD > 1) {
         if (blockIdx.x == 0 && threadIdx.x < WORLD && threadIdx.x != rank)
@@ -810,6 +839,7 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
 
     // a7: "1st synchronization" (as in gdraa_kernel)
     if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(2);
+    GDRAA_STAMP_DONE();
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (WORLD > 1) fence_acq_rel_sys();
     __syncthreads();

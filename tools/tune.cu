@@ -105,7 +105,9 @@ void run(void (*fn)(KParams), int threads, int smem, int gx, const char *kernel,
         std::fprintf(stderr, "timeout reported\n");
         std::exit(2);
     }
-    double acc[5] = {0, 0, 0, 0, 0};
+    // stamps: 0 start, 1 entry passed, 5 first CTA data done, 6 last CTA data done,
+    // 3 last CTA arrived (after its fence), 4 exit barrier passed
+    double acc[6] = {0, 0, 0, 0, 0, 0};
     int cnt = 0;
     for (int d = 0; d < WORLD; ++d) {
         std::vector<uint64_t> h(64 * kMaxWorld * 8);
@@ -115,11 +117,13 @@ void run(void (*fn)(KParams), int threads, int smem, int gx, const char *kernel,
             const uint64_t *a = &h[(e * kMaxWorld) * 8];
             const uint64_t *b = &h[(((e + 1) % 64) * kMaxWorld) * 8];
             if (!a[0] || !a[4] || !b[0] || b[0] < a[4] || b[0] - a[4] > 1000000) continue;
+            if (a[5] == ~0ull || a[6] < a[5] || a[5] < a[1]) continue;
             acc[0] += a[1] - a[0];
-            acc[1] += a[2] - a[1];
-            acc[2] += a[3] - a[2];
-            acc[3] += a[4] - a[3];
-            acc[4] += b[0] - a[4];
+            acc[1] += a[5] - a[1];
+            acc[2] += a[6] - a[5];
+            acc[3] += a[3] - a[6];
+            acc[4] += a[4] - a[3];
+            acc[5] += b[0] - a[4];
             ++cnt;
         }
     }
@@ -131,11 +135,11 @@ void run(void (*fn)(KParams), int threads, int smem, int gx, const char *kernel,
     std::printf("{\"world\": %d, \"L\": %zu, \"dtype\": \"%s\", \"mode\": \"%s\", \"kernel\": "
                 "\"%s\", \"shape\": \"%s\", \"threads\": %d, \"smem\": %d, \"grid\": %d, "
                 "\"us\": %.2f, \"gbs_per_rank\": %.1f, \"phase_us\": {\"entry\": %.2f, "
-                "\"data_cta0\": %.2f, \"to_last_arrival\": %.2f, \"exit\": %.2f, "
-                "\"gap_to_next\": %.2f}}\n",
+                "\"data_first_cta\": %.2f, \"cta_spread\": %.2f, \"drain\": %.2f, "
+                "\"exit\": %.2f, \"gap_to_next\": %.2f}}\n",
                 WORLD, L, sg == 4 ? "f32" : "bf16", MODE == kSgd ? "sgd" : "mean", kernel,
                 shape.c_str(), threads, smem, gx, t * 1e6, bytes / t / 1e9, ph(0), ph(1), ph(2),
-                ph(3), ph(4));
+                ph(3), ph(4), ph(5));
     std::fflush(stdout);
     for (int d = 0; d < WORLD; ++d) {
         CK(cudaSetDevice(d));
@@ -187,7 +191,7 @@ void sweep() {
     using S = Shape<TG, WORLD, MODE>;
     if (WHAT == "lib") {
         lsu<TG, WORLD, MODE, S::U, S::THREADS, S::MINB>();
-        tma<TG, WORLD, MODE, 8, 4>();
+        tma<TG, WORLD, MODE, 16, 4>();
     } else if (WHAT == "lsu") {
         lsu<TG, WORLD, MODE, 1, 512, 2>();
         lsu<TG, WORLD, MODE, 2, 512, 2>();
