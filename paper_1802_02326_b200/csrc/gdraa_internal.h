@@ -62,6 +62,8 @@ struct KParams {
     uint64_t ll_pairs;                       // capacity in 8-byte payload pairs per sender
     ErrBlock *err;                           // host-mapped (device alias)
     volatile uint64_t *done[kMaxWorld];      // host-mapped done flags (device alias) or null
+    const volatile int32_t *abort;           // host-mapped job-server abort flag, or null:
+                                             // spins give up early once a rank has died
 #ifdef GDRAA_TRACE
     uint64_t *trace;                         // tools/tune.cu only: %globaltimer stamps
 #endif

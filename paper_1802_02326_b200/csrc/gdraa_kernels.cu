@@ -83,13 +83,17 @@ __device__ __forceinline__ void st_vec(uint2 *p, uint2 v) {
     asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
 }
 
-// Spin until *flag >= target, bounded by timeout_ns of %globaltimer.
+// Spin until *flag >= target, bounded by timeout_ns of %globaltimer, and abandoned early
+// if the job server has flagged a dead rank (host-mapped, read every 4096 polls).
 __device__ __forceinline__ bool wait_geq(const uint64_t *flag, uint64_t target,
-                                         uint64_t timeout_ns) {
+                                         uint64_t timeout_ns,
+                                         const volatile int32_t *abort = nullptr) {
     if (ld_relaxed_sys(flag) < target) {
         const uint64_t t0 = global_timer_ns();
+        uint32_t polls = 0;
         while (ld_relaxed_sys(flag) < target) {
             if (global_timer_ns() - t0 > timeout_ns) return false;
+            if (abort != nullptr && (++polls & 4095u) == 0 && *abort != 0) return false;
         }
     }
     (void)ld_acquire_sys(flag);   // acquire pattern: orders our later reads after it
@@ -257,7 +261,7 @@ gdraa_kernel(const __grid_constant__ KParams p) {
             st_release_sys(&p.pad[vr][threadIdx.x]->entry[rank], epoch);
         __syncthreads();
         if (threadIdx.x < WORLD && threadIdx.x != rank) {
-            if (!wait_geq(&mine->entry[threadIdx.x], epoch, p.timeout_ns)) {
+            if (!wait_geq(&mine->entry[threadIdx.x], epoch, p.timeout_ns, p.abort)) {
                 report_timeout(p.err, 1, threadIdx.x, vr);
                 s_abort = 1;
             }
@@ -426,7 +430,7 @@ gdraa_kernel(const __grid_constant__ KParams p) {
         if (threadIdx.x < WORLD && threadIdx.x != rank)
             st_release_sys(&p.pad[vr][threadIdx.x]->exit[rank], epoch);
         if (threadIdx.x < WORLD && threadIdx.x != rank) {
-            if (!wait_geq(&mine->exit[threadIdx.x], epoch, p.timeout_ns)) {
+            if (!wait_geq(&mine->exit[threadIdx.x], epoch, p.timeout_ns, p.abort)) {
                 report_timeout(p.err, 2, threadIdx.x, vr);
                 s_abort = 1;
             }
@@ -557,7 +561,8 @@ gdraa_ll_kernel(const __grid_constant__ KParams p) {
                 const uint64_t t0 = global_timer_ns();
                 do {
                     r = ld_ll(src);
-                    if (global_timer_ns() - t0 > p.timeout_ns) {
+                    if (global_timer_ns() - t0 > p.timeout_ns ||
+                        (p.abort != nullptr && *p.abort != 0)) {
                         report_timeout(p.err, 1, q, vr);
                         ok = false;
                         break;
@@ -678,7 +683,7 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
             st_release_sys(&p.pad[vr][threadIdx.x]->entry[rank], epoch);
         __syncthreads();
         if (threadIdx.x < WORLD && threadIdx.x != rank) {
-            if (!wait_geq(&mine->entry[threadIdx.x], epoch, p.timeout_ns)) {
+            if (!wait_geq(&mine->entry[threadIdx.x], epoch, p.timeout_ns, p.abort)) {
                 report_timeout(p.err, 1, threadIdx.x, vr);
                 s_abort = 1;
             }
@@ -855,7 +860,7 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
         if (threadIdx.x < WORLD && threadIdx.x != rank)
             st_release_sys(&p.pad[vr][threadIdx.x]->exit[rank], epoch);
         if (threadIdx.x < WORLD && threadIdx.x != rank) {
-            if (!wait_geq(&mine->exit[threadIdx.x], epoch, p.timeout_ns)) {
+            if (!wait_geq(&mine->exit[threadIdx.x], epoch, p.timeout_ns, p.abort)) {
                 report_timeout(p.err, 2, threadIdx.x, vr);
                 s_abort = 1;
             }

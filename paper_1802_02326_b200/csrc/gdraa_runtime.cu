@@ -140,6 +140,7 @@ struct State {
     uint64_t ll_pairs = 0;
     ErrBlock *err_h = nullptr, *err_d = nullptr;
     volatile uint64_t *done_d = nullptr;
+    const volatile int32_t *abort_d = nullptr;   // device alias of the page's abort flag
     std::vector<Registration> regs;
     std::map<std::pair<int, std::string>, void *> opened;   // (peer, handle) -> base
     uint32_t reg_seq = 0;
@@ -278,6 +279,13 @@ int ipc_exchange(void *ptr, size_t bytes, uint64_t n, int dtype, int what,
 int check_sticky() {
     if (!g.inited) return fail(GDRAA_ESTATE, "gdraa_init has not been called");
     if (g.fatal) return fail(g.fatal_code, "%s", g.fatal_msg.c_str());
+    // a rank the job server saw die explains a device-side give-up: report it first
+    if (g.page != nullptr && !g.page_owned && g.page->abort) {
+        g.fatal = true;
+        g.fatal_code = GDRAA_EJOBSERVER;
+        g.fatal_msg = "job server reports rank " + std::to_string(g.page->dead_rank) + " died";
+        return fail(GDRAA_EJOBSERVER, "%s", g.fatal_msg.c_str());
+    }
     if (g.err_h != nullptr && g.err_h->code != 0) {
         std::string miss;
         for (int p = 0; p < kMaxWorld; ++p)
@@ -291,12 +299,6 @@ int check_sticky() {
         g.fatal_code = GDRAA_ETIMEOUT;
         g.fatal_msg = buf;
         return fail(GDRAA_ETIMEOUT, "%s", buf);
-    }
-    if (g.page != nullptr && !g.page_owned && g.page->abort) {
-        g.fatal = true;
-        g.fatal_code = GDRAA_EJOBSERVER;
-        g.fatal_msg = "job server reports rank " + std::to_string(g.page->dead_rank) + " died";
-        return fail(GDRAA_EJOBSERVER, "%s", g.fatal_msg.c_str());
     }
     return GDRAA_OK;
 }
@@ -335,6 +337,7 @@ void fill_common(KParams &p, uint64_t n) {
     p.ll_pairs = g.ll_pairs;
     p.err = g.err_d;
     p.done[0] = g.done_d;
+    p.abort = g.abort_d;
 }
 
 // Lemma 1/2 accounting of one call (s_w: bytes per broadcast element; 0 = same as g).
@@ -605,6 +608,7 @@ int gdraa_init(int world, int rank) {
     void *pd = nullptr;
     CUDA_TRY(cudaHostGetDevicePointer(&pd, g.page, 0));
     g.done_d = &static_cast<proto::ShmPage *>(pd)->done[rank];
+    g.abort_d = &static_cast<proto::ShmPage *>(pd)->abort;
 
     // Exchange signal pads (registration sequence 1).
     void *peers[kMaxWorld] = {};

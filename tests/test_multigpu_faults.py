@@ -1,0 +1,100 @@
+"""Failure handling over real processes (>= 2 GPUs): a peer that never arrives makes the
+kernel give up after GDRAA_TIMEOUT_MS and every later call report GDRAA_ETIMEOUT naming
+the missing rank ("peer-timeout ... names the missing ranks"); a peer process that
+dies is seen by the job server (socket EOF), whose abort flag -- mapped into the
+kernel's spin loops -- ends the wait long before the timeout (GDRAA_EJOBSERVER)."""
+import json
+import os
+import time
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from tests.conftest import has_cuda
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu,
+              pytest.mark.skipif(not has_cuda() or torch.cuda.device_count() < 2,
+                                 reason="needs >= 2 GPUs")]
+
+
+def _setup(rank, world, sock, timeout_ms):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["GDRAA_JOBSERVER"] = sock
+    os.environ["GDRAA_TIMEOUT_MS"] = str(timeout_ms)
+    torch.cuda.set_device(rank)
+    from paper_1802_02326_b200 import gdraa
+    gdraa.gdraa_init(world, rank)
+    dev = f"cuda:{rank}"
+    w = torch.zeros(1 << 20, device=dev)
+    g = torch.ones(1 << 20, device=dev)
+    v = torch.zeros(1 << 20, device=dev)
+    gdraa.gdraa_register(w)
+    gdraa.gdraa_register(g)
+    return gdraa, w, g, v
+
+
+def _timeout_worker(rank, world, sock, out, mode):
+    # rank 0 gives up after 1.5 s when the peer just skips the call; when the peer dies
+    # it keeps a 60 s timeout, so only the job server's abort flag can end its wait early
+    gdraa, w, g, v = _setup(rank, world, sock, 1500 if rank == 0 and mode == "skip" else 60000)
+    res = {"rank": rank}
+    if rank == 0:
+        t0 = time.time()
+        gdraa.gdraa_sgd_step(w, g, v, 0.1, 0.9)        # the peer never arrives
+        torch.cuda.synchronize()                         # kernel gives up after 1.5 s
+        res["kernel_s"] = time.time() - t0
+        try:
+            gdraa.gdraa_sgd_step(w, g, v, 0.1, 0.9)
+            res["second"] = "ok"
+        except gdraa.GdraaError as e:
+            res["second"] = e.name
+            res["msg"] = str(e)
+        try:
+            gdraa.gdraa_finalize()
+            res["finalize"] = "ok"
+        except gdraa.GdraaError as e:
+            res["finalize"] = e.name
+    else:
+        if mode == "die":
+            time.sleep(1.0)
+            os._exit(3)                                  # dies without finalize
+        time.sleep(4.0)                                  # alive, but skips the call
+        gdraa.gdraa_finalize()
+        res["finalize"] = "ok"
+    with open(os.path.join(out, f"r{rank}.json"), "w") as f:
+        json.dump(res, f)
+
+
+def _run(tmp_path, mode):
+    from paper_1802_02326_b200 import jobserver
+    world = 2
+    sock = str(tmp_path / "js.sock")
+    js = jobserver.start(world, sock)
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_timeout_worker, args=(r, world, sock, str(tmp_path), mode))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    out, err = js.communicate(timeout=60)
+    return [p.exitcode for p in procs], json.load(open(tmp_path / "r0.json")), out
+
+
+def test_peer_timeout_names_missing_rank(tmp_path):
+    codes, r0, _ = _run(tmp_path, "skip")
+    assert codes == [0, 0], codes
+    assert 1.0 < r0["kernel_s"] < 20, r0
+    assert r0["second"] == "GDRAA_ETIMEOUT" and "missing rank(s) 1" in r0["msg"], r0
+    assert r0["finalize"] == "GDRAA_ETIMEOUT", r0
+
+
+def test_dead_rank_aborts_the_wait(tmp_path):
+    # rank 0's kernel would wait 60 s; the job server's abort flag ends it in seconds
+    codes, r0, js_out = _run(tmp_path, "die")
+    assert codes[1] == 3 and codes[0] == 0, codes
+    assert r0["kernel_s"] < 15, r0
+    assert r0["second"] == "GDRAA_EJOBSERVER" and "rank 1" in r0["msg"], r0
+    assert "disconnected" in js_out
