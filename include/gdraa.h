@@ -198,6 +198,25 @@ int gdraa_shard(int world, int rank, size_t n, size_t *off, size_t *len);
  */
 size_t gdraa_small_message_bytes(int world);
 
+/*
+ * gdraa_small_step_bytes -- the largest gradient payload (n * sizeof(g), bytes per rank)
+ * that gdraa_sgd_step / _ex / _mp (and their _range forms, per range) serve with the
+ * small-message SGD kernel at this world size.  That kernel follows the paper's own
+ * data flow: every rank pushes block D(r, q) into owner q's receive slot as
+ * 16-byte entries carrying the call's epoch flag (Fig. 3a), the owner folds in rank
+ * order, divides once, applies the update and pushes the updated block into every
+ * rank's slot the same way (Fig. 3b), and every rank copies the blocks it receives into
+ * its w.  The arrival of the entries is both synchronisations: no device barrier runs
+ * and no rank touches another rank's g or w.  The result -- w' everywhere, v' on the
+ * owner shard, g unchanged -- is bitwise the two-shot kernel's.
+ *   world: 2..GDRAA_MAX_WORLD (0 otherwise); dtype: of g (GDRAA_F32 / GDRAA_BF16);
+ *   mixed: nonzero for gdraa_sgd_step_mp (bf16 broadcast).
+ * Default limit 2 MiB / (world - 1) (GDRAA_LL_SGD_MAX_BYTES overrides, 0 disables),
+ * lowered to what one sender's receive slot (gdraa_small_message_bytes) can hold.
+ * Pure host function.
+ */
+size_t gdraa_small_step_bytes(int world, int dtype, int mixed);
+
 typedef struct {
     uint64_t calls;            /* collective calls completed on the device (device counter) */
     uint64_t sync_waits;       /* device barrier completions: 2 per call when world >= 2     */
@@ -208,10 +227,10 @@ typedef struct {
     uint64_t adds;             /* aggregation adds (Eq. 3, first term)                       */
     uint64_t divides;          /* aggregation divides (Eq. 3, second term)                   */
     uint64_t launches;         /* kernels launched by this library                           */
-    uint64_t ll_calls;         /* allreduce_mean calls served by the small-message path, whose
-                                  synchronisation travels with the data (no device barrier;
-                                  not counted in sync_waits; GDRAA_LL_MAX_BYTES, default
-                                  262144, 0 disables)                                        */
+    uint64_t ll_calls;         /* calls served by a small-message path (allreduce_mean below
+                                  gdraa_small_message_bytes, sgd_step below
+                                  gdraa_small_step_bytes), whose synchronisation travels
+                                  with the data (no device barrier; not in sync_waits)       */
 } gdraa_stats_t;
 
 /*

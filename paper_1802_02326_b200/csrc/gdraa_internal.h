@@ -94,11 +94,23 @@ bool use_tma_kernel(int dtype, int mode, int world);
 cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool cooperative,
                             cudaStream_t s);
 
+// Small-message fused SGD step (kSgd / kSgdMp): gradient blocks and updated blocks travel
+// as LL entries through the same receive areas; the data carries both synchronisations.
+// Requires ll_sgd_fits(p.blk, ...).
+cudaError_t launch_gdraa_ll_sgd(const KParams &p, int dtype, int mode, int vr_rows,
+                                bool cooperative, cudaStream_t s);
+// Whether a shard of blk elements fits one sender's LL slot (gradient + broadcast part).
+bool ll_sgd_fits(uint64_t blk, int dtype, int mode, uint64_t ll_pairs);
+// Largest gdraa_sgd_step gradient payload (n * sizeof(g), bytes per rank) served by the
+// small-message SGD path (GDRAA_LL_SGD_MAX_BYTES overrides, 0 disables).
+uint64_t ll_sgd_limit_bytes(int world);
+
 // Largest allreduce_mean payload (bytes per rank) served by the LL path: the measured
 // crossover with the two-shot kernel is ~4 MiB at N=2 and ~1.5 MiB at N=4
 // (profiles/r15_sweep*_ll*.jsonl), i.e. ~4 MiB / (N-1) as the LL bytes grow with N-1.
 // GDRAA_LL_MAX_BYTES overrides it (0 disables the LL path).
 uint64_t ll_limit_bytes(int world);
 constexpr uint64_t kLLBaseBytes = 4ull << 20;
+constexpr uint64_t kLLSgdBaseBytes = 2ull << 20;
 
 }  // namespace gdraa

@@ -474,6 +474,26 @@ __device__ __forceinline__ uint4 ld_ll(const uint4 *p) {
     return r;
 }
 
+// Poll one LL entry until both flag words carry `flag`.  Bounded by timeout_ns; the
+// host-mapped abort flag is read only every 1024 polls (a read per poll from thousands
+// of polling threads would queue on PCIe and serialise the whole kernel).
+__device__ __forceinline__ uint4 ll_wait(const uint4 *src, uint32_t flag, uint64_t timeout_ns,
+                                         const volatile int32_t *abort, bool &ok) {
+    uint4 r = ld_ll(src);
+    if (r.y == flag && r.w == flag) return r;
+    const uint64_t t0 = global_timer_ns();
+    uint32_t polls = 0;
+    do {
+        r = ld_ll(src);
+        if ((++polls & 1023u) == 0 &&
+            (global_timer_ns() - t0 > timeout_ns || (abort != nullptr && *abort != 0))) {
+            ok = false;
+            break;
+        }
+    } while (r.y != flag || r.w != flag);
+    return r;
+}
+
 // 8 payload bytes of the buffer at pair j (fewer at the ragged end; the rest is 0).
 __device__ __forceinline__ uint2 load_pair(const void *buf, uint64_t j, uint64_t nbytes) {
     const uint64_t b0 = j * 8;
@@ -556,18 +576,10 @@ gdraa_ll_kernel(const __grid_constant__ KParams p) {
                 continue;
             }
             const uint4 *src = p.ll[vr][rank] + (par * WORLD + q) * p.ll_pairs + j;
-            uint4 r = ld_ll(src);
-            if (r.y != flag || r.w != flag) {
-                const uint64_t t0 = global_timer_ns();
-                do {
-                    r = ld_ll(src);
-                    if (global_timer_ns() - t0 > p.timeout_ns ||
-                        (p.abort != nullptr && *p.abort != 0)) {
-                        report_timeout(p.err, 1, q, vr);
-                        ok = false;
-                        break;
-                    }
-                } while (r.y != flag || r.w != flag);
+            const uint4 r = ll_wait(src, flag, p.timeout_ns, p.abort, ok);
+            if (!ok) {
+                report_timeout(p.err, 1, q, vr);
+                break;
             }
             w0[q] = r.x;
             w1[q] = r.z;
@@ -576,6 +588,185 @@ gdraa_ll_kernel(const __grid_constant__ KParams p) {
         store_pair(buf, j, nbytes,
                    make_uint2(WordMean<TG, WORLD>::run(w0), WordMean<TG, WORLD>::run(w1)));
     }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&mine->arrive, 1u);
+        s_last = (prev == gridDim.x - 1);
+        if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        mine->arrive = 0;
+        mine->calls += 1;
+        mine->ll_calls += 1;
+        mine->epoch = epoch;
+        if (p.done[vr] != nullptr) *p.done[vr] = epoch;
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// Small-message fused SGD step (the latency path of gdraa_sgd_step / _mp).  The
+// momentum is owner-sharded (AMB-19), so the one-shot scheme above cannot serve it; this
+// kernel keeps the two-shot structure of Algorithm 1 but lets the data carry the
+// synchronisations, as the paper's RDMA writes into the receive buffer RB do:
+//   A  "Reduce": rank r PUSHES its block D(r, q) into owner q's receive slot [par][r]
+//      as LL entries {word, flag, word, flag} (Fig. 3a);
+//   B  "Aggregation" + update: the owner polls the N-1 entries of each position (its
+//      own block comes from local HBM), folds them in ascending rank, divides once, and
+//      applies the momentum step; it stores v', w' locally and pushes w'
+//      (bf16 RNE(w') for _mp) into every peer's slot [par][r] behind the RS part
+//      (Fig. 3b);
+//   C  every rank polls the broadcast entries of each peer's block and writes them into
+//      its own w (or bf16 model copy).
+// Arrival of an entry is the 2nd synchronisation for that position; the arrival of the
+// last broadcast entry is the 1st.  No rank ever reads or writes another rank's g or w,
+// so neither barrier of the two-shot kernel is needed.  Slot reuse: rank 0 owns a
+// non-empty block whenever n >= 1, so finishing call e-1 means having received rank 0's
+// broadcast, which rank 0 sent after receiving every rank's call e-1 block, which every
+// rank sent after finishing call e-2 -- so parity (e & 1) is free again at call e.
+// Slot layout per sender: pairs [0, rs_cap) = the sender's gradient block, pairs
+// [rs_cap, rs_cap + ag_cap) = the sender's updated block (caps from the padded shard).
+// Work unit of phase B: 4 consecutive elements = 16 (fp32) / 8 (bf16) gradient bytes.
+// ---------------------------------------------------------------------------------
+template <typename TG, int WORLD, int MODE>
+__global__ void __launch_bounds__(512, 2)
+gdraa_ll_sgd_kernel(const __grid_constant__ KParams p) {
+    using EL = Elem<TG>;
+    using Raw = typename EL::Raw;
+    constexpr uint64_t SG = sizeof(TG);
+    constexpr uint64_t SW = MODE == kSgdMp ? 2 : 4;          // broadcast bytes / element
+    constexpr int RS_PAIRS = static_cast<int>(SG * E / 8);    // 2 (fp32) or 1 (bf16)
+    constexpr int AG_PAIRS = static_cast<int>(SW * E / 8);    // 2 (fp32 w') or 1 (bf16)
+    const int vr = blockIdx.y;
+    const int rank = p.rank0 + vr;
+    Pad *mine = p.pad[vr][rank];
+    __shared__ int s_last;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint64_t epoch = *reinterpret_cast<volatile uint64_t *>(&mine->epoch) + 1;
+    const uint32_t flag = static_cast<uint32_t>(epoch);
+    const uint64_t par = epoch & 1u;
+    const uint64_t rs_cap = (p.blk * SG + 7) / 8;   // the runtime checks rs + ag caps fit
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    auto shard = [&](int q, uint64_t &o, uint64_t &l) {
+        o = min(static_cast<uint64_t>(q) * p.blk, p.n);
+        l = min(p.blk, p.n - o);
+    };
+    const TG *const gl = static_cast<const TG *>(p.src[vr][rank]);
+    // our receive slot from sender q, and sender rank's slot in peer q's area
+    auto rx = [&](int q) { return p.ll[vr][rank] + (par * WORLD + q) * p.ll_pairs; };
+    auto tx = [&](int q) { return p.ll[vr][q] + (par * WORLD + rank) * p.ll_pairs; };
+    // poll one entry until it carries this call's flag (bounded; abandons on abort)
+    bool ok = true;
+    auto poll = [&](const uint4 *src, int q, int phase) -> uint2 {
+        const uint4 r = ll_wait(src, flag, p.timeout_ns, p.abort, ok);
+        if (!ok) report_timeout(p.err, phase, q, vr);
+        return make_uint2(r.x, r.z);
+    };
+
+    // A: push block D(rank, q) to every owner q != rank.
+#pragma unroll 1
+    for (int k = 1; k < WORLD; ++k) {
+        const int q = (rank + k) % WORLD;
+        uint64_t oq, lq;
+        shard(q, oq, lq);
+        const uint64_t nb = lq * SG, np = (nb + 7) / 8;
+        const void *base = gl + oq;
+        uint4 *dstq = tx(q);
+        for (uint64_t j = tid; j < np; j += stride) {
+            const uint2 w = load_pair(base, j, nb);
+            st_ll(dstq + j, make_uint4(w.x, flag, w.y, flag));
+        }
+    }
+
+    // B: fold + update our block, push w' to every peer.
+    uint64_t off, len;
+    shard(rank, off, len);
+    float *const vloc = p.v[vr];
+    float *const wloc = MODE == kSgdMp ? p.wm[vr] : static_cast<float *>(p.dst[vr][rank]);
+    const float lr = p.lr, mom = p.mom, wd = p.wd;
+    const uint64_t nunits = (len + E - 1) / E;
+    for (uint64_t u = tid; ok && u < nunits; u += stride) {
+        const uint64_t i0 = u * E;                       // first element (shard-relative)
+        const int cnt = static_cast<int>(len - i0 < E ? len - i0 : E);
+        const int rs_n = static_cast<int>((cnt * SG + 7) / 8);   // RS pairs of this unit
+        float x[WORLD][E];
+#pragma unroll
+        for (int q = 0; q < WORLD; ++q) {
+            if (q == rank) {
+                for (int e = 0; e < E; ++e) x[q][e] = e < cnt ? EL::load1(gl, off + i0 + e) : 0.f;
+                continue;
+            }
+            uint32_t wd4[4] = {0u, 0u, 0u, 0u};
+            const uint4 *src = rx(q) + u * RS_PAIRS;
+            for (int h = 0; h < rs_n; ++h) {
+                const uint2 pr = poll(src + h, q, 1);
+                wd4[2 * h] = pr.x;
+                wd4[2 * h + 1] = pr.y;
+            }
+            Raw raw;
+            if constexpr (std::is_same<TG, float>::value)
+                raw = make_uint4(wd4[0], wd4[1], wd4[2], wd4[3]);
+            else
+                raw = make_uint2(wd4[0], wd4[1]);
+            EL::widen(raw, x[q]);
+        }
+        if (!ok) break;
+        float wv[E], vv[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if (e < cnt) {
+                float col[WORLD];
+#pragma unroll
+                for (int q = 0; q < WORLD; ++q) col[q] = x[q][e];
+                const float m = average<WORLD>(col);
+                wv[e] = wloc[off + i0 + e];
+                vv[e] = vloc[off + i0 + e];
+                sgd(m, lr, mom, wd, wv[e], vv[e]);
+                vloc[off + i0 + e] = vv[e];
+                wloc[off + i0 + e] = wv[e];
+                if (MODE == kSgdMp)
+                    Elem<__nv_bfloat16>::store1(p.dst[vr][rank], off + i0 + e, wv[e]);
+            } else {
+                wv[e] = 0.f;
+            }
+        }
+        // broadcast entries of this unit (fp32 w': 2 pairs, bf16 copy: 1 pair)
+        uint32_t ow[4];
+        if (MODE == kSgdMp) {
+            const uint2 b = Elem<__nv_bfloat16>::narrow(wv);
+            ow[0] = b.x; ow[1] = b.y; ow[2] = 0u; ow[3] = 0u;
+        } else {
+            ow[0] = __float_as_uint(wv[0]); ow[1] = __float_as_uint(wv[1]);
+            ow[2] = __float_as_uint(wv[2]); ow[3] = __float_as_uint(wv[3]);
+        }
+        const int ag_n = static_cast<int>((cnt * SW + 7) / 8);
+#pragma unroll
+        for (int k = 1; k < WORLD; ++k) {
+            uint4 *dstq = tx((rank + k) % WORLD) + rs_cap + u * AG_PAIRS;
+            for (int h = 0; h < ag_n; ++h)
+                st_ll(dstq + h, make_uint4(ow[2 * h], flag, ow[2 * h + 1], flag));
+        }
+    }
+
+    // C: receive every peer's updated block into our w (or bf16 model copy).
+    void *const wdst = p.dst[vr][rank];
+#pragma unroll 1
+    for (int k = 1; ok && k < WORLD; ++k) {
+        const int q = (rank + k) % WORLD;
+        uint64_t oq, lq;
+        shard(q, oq, lq);
+        const uint64_t nb = lq * SW, np = (nb + 7) / 8;
+        void *base = static_cast<char *>(wdst) + oq * SW;
+        const uint4 *src = rx(q) + rs_cap;
+        for (uint64_t j = tid; j < np; j += stride) {
+            const uint2 w = poll(src + j, q, 2);
+            if (!ok) break;
+            store_pair(base, j, nb, w);
+        }
+    }
+
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -637,8 +828,17 @@ __device__ __forceinline__ void bulk_g2s(void *smem, const void *gmem, uint32_t 
 // Stage = one chunk of CH elements of every source (+ w, v): about STAGE_KB per stage.
 // 16 consumer warps: same rate as 8 on the full grid, and 607 GB/s (full rate) from only
 // 64 SMs at N=2 vs 595 for 8 warps (profiles/r21_ctas_n2.jsonl).
-template <typename TG, int WORLD, int MODE, int CW_ = 16, int ST_ = 4, int STAGE_KB = 40>
+// End game: the last ~2 waves of chunks are CH / TAILDIV elements, and while they are
+// handed out a producer keeps at most TDEPTH of them in flight (so no CTA sits on a
+// deep private queue while others have run dry).
+// ROT: the producer issues the N gradient copies of a chunk starting at its own rank
+// (rank, rank+1, ...) instead of rank 0 (the fold order is unaffected).
+template <typename TG, int WORLD, int MODE, int CW_ = 16, int ST_ = 4, int TAILDIV_ = 4,
+          int TDEPTH_ = ST_, int ROT_ = 0, int STAGE_KB = 40>
 struct TmaCfg {
+    static constexpr int TAILDIV = TAILDIV_;
+    static constexpr bool ROT = ROT_ != 0;
+    static constexpr int TDEPTH = TDEPTH_ < ST_ ? TDEPTH_ : ST_;
     static constexpr int SG = sizeof(TG);
     static constexpr bool UPD = MODE != kMean;
     static constexpr int PER_EL = WORLD * SG + (UPD ? 8 : 0);      // smem bytes / element
@@ -651,10 +851,11 @@ struct TmaCfg {
     static constexpr int SMEM = STAGES * STAGE_BYTES;
 };
 
-template <typename TG, int WORLD, int MODE, int CW_ = 16, int ST_ = 4>
-__global__ void __launch_bounds__(TmaCfg<TG, WORLD, MODE, CW_, ST_>::THREADS, 1)
+template <typename TG, int WORLD, int MODE, int CW_ = 16, int ST_ = 4, int TAILDIV_ = 4,
+          int TDEPTH_ = ST_, int ROT_ = 0>
+__global__ void __launch_bounds__(TmaCfg<TG, WORLD, MODE, CW_, ST_, TAILDIV_, TDEPTH_, ROT_>::THREADS, 1)
 gdraa_tma_kernel(const __grid_constant__ KParams p) {
-    using C = TmaCfg<TG, WORLD, MODE, CW_, ST_>;
+    using C = TmaCfg<TG, WORLD, MODE, CW_, ST_, TAILDIV_, TDEPTH_, ROT_>;
     using EL = Elem<TG>;
     using Raw = typename EL::Raw;
     constexpr bool kUpdate = C::UPD;
@@ -696,9 +897,9 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     const uint64_t off = min(static_cast<uint64_t>(rank) * p.blk, p.n);
     const uint64_t len = min(p.blk, p.n - off);
     const uint64_t lenv = len & ~7ull;                  // bulk copies: 16-byte multiples
-    // Chunks of CH elements, the last ~2 waves of CH/4 so the CTAs finish together (the
-    // end-game of the LSU kernel); chunk c -> (e0, n_el) is a pure function.
-    constexpr uint64_t CHS = C::CH / 4;
+    // Chunks of CH elements, the last ~2 waves of CH/TAILDIV so the CTAs finish together
+    // (the end-game of the LSU kernel); chunk c -> (e0, n_el) is a pure function.
+    constexpr uint64_t CHS = C::CH / C::TAILDIV;
     const uint64_t tailv = 2ull * gridDim.x * CHS;
     const uint64_t nbig = lenv > tailv ? (lenv - tailv) / C::CH : 0;
     const uint64_t small0 = nbig * C::CH;
@@ -728,10 +929,17 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     if (warp == 0) {
         // producer: a3 loads (and the local w, v) of one chunk per stage
         if (lane == 0) {
+            bool tail = false;
             for (uint32_t it = 0;; ++it) {
                 const int s = it % C::STAGES;
                 if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+                if (C::TDEPTH < C::STAGES && tail && it >= C::TDEPTH) {
+                    // end game: wait until stage it - TDEPTH has been consumed
+                    const uint32_t j = it - C::TDEPTH;
+                    mbar_wait(&empty[j % C::STAGES], (j / C::STAGES) & 1);
+                }
                 const uint32_t c = atomicAdd(&mine->next, 1u);
+                tail = c >= nbig;
                 if (c >= nchunks) {
                     s_chunk[s] = 0xFFFFFFFFu;
                     mbar_arrive(&full[s]);
@@ -743,9 +951,11 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
                 chunk(c, e0, n_el);
                 mbar_arrive_tx(&full[s], n_el * C::PER_EL);
 #pragma unroll
-                for (int q = 0; q < WORLD; ++q)
+                for (int k = 0; k < WORLD; ++k) {
+                    const int q = C::ROT ? (rank + k) % WORLD : k;
                     bulk_g2s(stage_src(s, q), static_cast<const TG *>(p.src[vr][q]) + off + e0,
                              n_el * C::SG, &full[s]);
+                }
                 if (kUpdate) {
                     bulk_g2s(stage_w(s), wloc + off + e0, n_el * 4, &full[s]);
                     bulk_g2s(stage_v(s), vloc + off + e0, n_el * 4, &full[s]);
@@ -1083,6 +1293,63 @@ cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool coope
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     uint64_t gx = (npairs + kT - 1) / kT;
     const uint64_t cap = static_cast<uint64_t>(sms) * 2 / vr_rows;   // all resident
+    if (gx > cap) gx = cap;
+    if (gx < 1) gx = 1;
+    dim3 grid(static_cast<unsigned>(gx), vr_rows), block(kT);
+    if (cooperative) {
+        void *args[] = {const_cast<KParams *>(&p)};
+        return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(fn), grid, block, args,
+                                           0, s);
+    }
+    return launch_pdl(fn, grid, block, s, p);
+}
+
+namespace {
+template <typename TG, int MODE>
+KernelFnLL pick_ll_sgd_m(int world) {
+    switch (world) {
+        case 2: return gdraa_ll_sgd_kernel<TG, 2, MODE>;
+        case 3: return gdraa_ll_sgd_kernel<TG, 3, MODE>;
+        case 4: return gdraa_ll_sgd_kernel<TG, 4, MODE>;
+        case 5: return gdraa_ll_sgd_kernel<TG, 5, MODE>;
+        case 6: return gdraa_ll_sgd_kernel<TG, 6, MODE>;
+        case 7: return gdraa_ll_sgd_kernel<TG, 7, MODE>;
+        case 8: return gdraa_ll_sgd_kernel<TG, 8, MODE>;
+        default: return nullptr;
+    }
+}
+}  // namespace
+
+bool ll_sgd_fits(uint64_t blk, int dtype, int mode, uint64_t ll_pairs) {
+    const uint64_t sg = dtype == GDRAA_F32 ? 4 : 2, sw = mode == kSgdMp ? 2 : 4;
+    return (blk * sg + 7) / 8 + (blk * sw + 7) / 8 <= ll_pairs;
+}
+
+cudaError_t launch_gdraa_ll_sgd(const KParams &p, int dtype, int mode, int vr_rows,
+                                bool cooperative, cudaStream_t s) {
+    KernelFnLL fn = nullptr;
+    if (mode == kSgd)
+        fn = dtype == GDRAA_F32 ? pick_ll_sgd_m<float, kSgd>(p.world)
+                                : pick_ll_sgd_m<__nv_bfloat16, kSgd>(p.world);
+    else if (mode == kSgdMp)
+        fn = dtype == GDRAA_F32 ? pick_ll_sgd_m<float, kSgdMp>(p.world)
+                                : pick_ll_sgd_m<__nv_bfloat16, kSgdMp>(p.world);
+    if (fn == nullptr) return cudaErrorInvalidValue;
+    if (!ll_sgd_fits(p.blk, dtype, mode, p.ll_pairs)) return cudaErrorInvalidValue;
+    constexpr int kT = 512;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kT, 0);
+    if (e != cudaSuccess) return e;
+    // every CTA polls entries other CTAs (and peers) produce: the grid must be resident
+    const uint64_t es = dtype == GDRAA_F32 ? 4 : 2;
+    const uint64_t work = (p.blk * es + 7) / 8 > (p.blk + E - 1) / E ? (p.blk * es + 7) / 8
+                                                                       : (p.blk + E - 1) / E;
+    uint64_t gx = (work + kT - 1) / kT;
+    const uint64_t cap = static_cast<uint64_t>(sms) * per_sm / vr_rows;
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
     dim3 grid(static_cast<unsigned>(gx), vr_rows), block(kT);

@@ -382,6 +382,12 @@ uint64_t ll_limit_bytes(int world) {
     return env_u64("GDRAA_LL_MAX_BYTES", dflt) / 8 * 8;
 }
 
+uint64_t ll_sgd_limit_bytes(int world) {
+    if (world < 2) return 0;
+    const uint64_t dflt = kLLSgdBaseBytes / static_cast<uint64_t>(world - 1);
+    return env_u64("GDRAA_LL_SGD_MAX_BYTES", dflt);
+}
+
 namespace {
 
 // One rank's LL receive area: [2 parities][world senders][pairs] x 16 bytes.
@@ -497,6 +503,12 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
         if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr LL launch: %s", cudaGetErrorString(e));
         return GDRAA_OK;
     }
+    if (upd && world > 1 && n * es <= ll_sgd_limit_bytes(world) &&
+        ll_sgd_fits(p.blk, dtype, mode, p.ll_pairs)) {   // small-message SGD step
+        cudaError_t e = launch_gdraa_ll_sgd(p, dtype, mode, world, true, s);
+        if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr LL SGD launch: %s", cudaGetErrorString(e));
+        return GDRAA_OK;
+    }
     int gx = 0;
     cudaError_t e = use_tma_kernel(dtype, mode, world)
                         ? launch_gdraa_tma(p, dtype, mode, world, true, s, &gx)
@@ -519,6 +531,23 @@ const char *gdraa_version(void) { return "gdraa 0.1.0 (sm_100a)"; }
 size_t gdraa_small_message_bytes(int world) {
     if (world < 1 || world > kMaxWorld) return 0;
     return static_cast<size_t>(ll_limit_bytes(world));
+}
+
+size_t gdraa_small_step_bytes(int world, int dtype, int mixed) {
+    if (world < 2 || world > kMaxWorld || (dtype != GDRAA_F32 && dtype != GDRAA_BF16)) return 0;
+    const uint64_t lim = ll_sgd_limit_bytes(world), pairs = ll_limit_bytes(world) / 8;
+    const uint64_t es = elem_size(dtype);
+    // largest n <= lim / es whose shard fits one sender's LL slot (blk grows with n)
+    const int mode = mixed ? kSgdMp : kSgd;
+    uint64_t lo = 0, hi = lim / es;
+    while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo + 1) / 2;
+        uint64_t blk, off, len;
+        partition(mid, world, 0, &blk, &off, &len);
+        if (ll_sgd_fits(blk, dtype, mode, pairs)) lo = mid; else hi = mid - 1;
+    }
+    const uint64_t n = lo;
+    return static_cast<size_t>(n * es);
 }
 
 int gdraa_shard(int world, int rank, size_t n, size_t *off, size_t *len) {
@@ -775,8 +804,17 @@ static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, 
     }
     p.v[0] = static_cast<float *>(offset_ptr(v, first, 4));
     p.wm[0] = mode == kSgdMp ? static_cast<float *>(offset_ptr(wm, first, 4)) : nullptr;
-    rc = launch(p, rg->dtype, mode, reinterpret_cast<cudaStream_t>(s));
-    if (rc) return rc;
+    if (g.ll != nullptr && count * eg <= ll_sgd_limit_bytes(g.world) &&
+        ll_sgd_fits(p.blk, rg->dtype, mode, g.ll_pairs)) {
+        // small message: the data carries both synchronisations (same result, bit for bit)
+        cudaError_t e = launch_gdraa_ll_sgd(p, rg->dtype, mode, 1, false,
+                                            reinterpret_cast<cudaStream_t>(s));
+        if (e != cudaSuccess) return fail(GDRAA_ECUDA, "LL SGD kernel launch: %s", cudaGetErrorString(e));
+        g.issued += 1;
+    } else {
+        rc = launch(p, rg->dtype, mode, reinterpret_cast<cudaStream_t>(s));
+        if (rc) return rc;
+    }
     account(count, rg->dtype, mode == kSgd ? 4 : 2);
     return GDRAA_OK;
 }

@@ -20,7 +20,7 @@ ERRORS = {0: "GDRAA_OK", -1: "GDRAA_EINVAL", -2: "GDRAA_ENOTREG", -3: "GDRAA_ESH
           -4: "GDRAA_ECUDA", -5: "GDRAA_ETIMEOUT", -6: "GDRAA_ESTATE", -7: "GDRAA_EJOBSERVER"}
 
 EXPORTED = ["gdraa_sgd_step_ex", "gdraa_sgd_step_mp", "gdraa_poly_lr",
-            "gdraa_small_message_bytes", "gdraa_allreduce_mean_range",
+            "gdraa_small_message_bytes", "gdraa_small_step_bytes", "gdraa_allreduce_mean_range",
             "gdraa_sgd_step_range", "gdraa_sgd_step_mp_range",
             "gdraa_vr_sgd_step_ex", "gdraa_vr_sgd_step_mp",
             "gdraa_init", "gdraa_register", "gdraa_deregister","gdraa_allreduce_mean", "gdraa_sgd_step",
@@ -66,6 +66,7 @@ _sig = {
     "gdraa_sgd_step_mp": ([_vp, _vp, _vp, _vp, _f, _f, _f, _vp], _i),
     "gdraa_poly_lr": ([_f, ctypes.c_uint64, ctypes.c_uint64, _f], _f),
     "gdraa_small_message_bytes": ([_i], _sz),
+    "gdraa_small_step_bytes": ([_i, _i, _i], _sz),
     "gdraa_allreduce_mean_range": ([_vp, _sz, _sz, _vp], _i),
     "gdraa_sgd_step_range": ([_vp, _vp, _vp, _sz, _sz, _f, _f, _f, _vp], _i),
     "gdraa_sgd_step_mp_range": ([_vp, _vp, _vp, _vp, _sz, _sz, _f, _f, _f, _vp], _i),
@@ -180,6 +181,10 @@ def gdraa_sgd_step_mp_range(w_master, w_model, g, v, first: int, count: int, lr:
 
 def gdraa_small_message_bytes(world: int) -> int:
     return int(_lib.gdraa_small_message_bytes(world))
+
+
+def gdraa_small_step_bytes(world: int, dtype: int = GDRAA_F32, mixed: bool = False) -> int:
+    return int(_lib.gdraa_small_step_bytes(world, dtype, 1 if mixed else 0))
 
 
 def gdraa_shard(world: int, rank: int, n: int):

@@ -104,3 +104,24 @@ def test_small_message_threshold():
         lim = gdraa.gdraa_small_message_bytes(n)
         assert lim % 8 == 0 and (4 << 20) // (n - 1) - 8 < lim <= (4 << 20) // (n - 1)
     assert gdraa.gdraa_small_message_bytes(9) == 0
+
+
+@pytest.mark.parametrize("mixed", [False, True])
+def test_small_step_threshold(mixed):
+    """Small-message SGD threshold: at most 2 MiB / (N-1) of gradient bytes, and the
+    largest n whose padded shard (gradient + broadcast part) fits one sender's slot."""
+    assert gdraa.gdraa_small_step_bytes(1) == 0 and gdraa.gdraa_small_step_bytes(9) == 0
+    for N in range(2, 9):
+        pairs = gdraa.gdraa_small_message_bytes(N) // 8
+        for code, sg in ((gdraa.GDRAA_F32, 4), (gdraa.GDRAA_BF16, 2)):
+            sw = 2 if mixed else 4
+            lim = gdraa.gdraa_small_step_bytes(N, code, mixed)
+            assert 0 < lim <= (2 << 20) // (N - 1) and lim % sg == 0
+
+            def fits(n):
+                blk = oracle.partition(n, N, 0, Q=64)[1]
+                return (blk * sg + 7) // 8 + (blk * sw + 7) // 8 <= pairs
+
+            n = lim // sg
+            assert fits(n)
+            assert n == (2 << 20) // (N - 1) // sg or not fits(n + 1)

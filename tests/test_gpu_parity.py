@@ -120,6 +120,84 @@ def test_vr_sgd_step(N, dt, family):
             assert np.array_equal(from_dev(g_d[r]), gs[r])
 
 
+@pytest.mark.parametrize("N", [2, 3, 4, 8])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("mixed", [False, True])
+def test_vr_sgd_latency_path(N, dt, mixed):
+    """The small-message SGD kernel (gradient and updated blocks pushed as flagged LL
+    entries, no device barrier): sizes on both sides of its threshold, ragged shards
+    (odd lengths, empty shards), 3 chained steps (epoch parity of the receive slots),
+    weight decay, and the mixed-precision broadcast."""
+    bf16 = dt == "bf16"
+    es = 2 if bf16 else 4
+    code = gdraa.GDRAA_BF16 if bf16 else gdraa.GDRAA_F32
+    lim = gdraa.gdraa_small_step_bytes(N, code, mixed) // es   # largest LL element count
+    assert lim > 0
+    for L in (1, 3, 63, 65, 127, 4097, 65_537, lim - 1, lim, lim + 1):
+        gs0 = make_grads("like", 900 + L % 13, N, L, bf16)
+        w, v = synth.w_like(901, L), synth.w_like(902, L)
+        w_d = [to_dev(w) for _ in range(N)]
+        v_d = [to_dev(v) for _ in range(N)]
+        mo_d = [torch.zeros(L, dtype=torch.bfloat16, device=DEV) for _ in range(N)]
+        for it in range(3):
+            gs = gs0 if it == 0 else make_grads("like", 910 + it, N, L, bf16)
+            g_d = [to_dev(g, bf16) for g in gs]
+            if mixed:
+                w, v, model = oracle.sgd_step_wd(gs, w, v, synth.PAPER_LR, synth.PAPER_MOM,
+                                                 0.001, model_dtype=oracle.BF16)
+                gdraa.gdraa_vr_sgd_step_mp(w_d, mo_d, g_d, v_d, synth.PAPER_LR,
+                                           synth.PAPER_MOM, 0.001)
+            else:
+                w, v = oracle.sgd_step_wd(gs, w, v, synth.PAPER_LR, synth.PAPER_MOM, 0.001)
+                gdraa.gdraa_vr_sgd_step_ex(w_d, g_d, v_d, synth.PAPER_LR, synth.PAPER_MOM,
+                                           0.001)
+            torch.cuda.synchronize()
+            for r in range(N):
+                off, ln = gdraa.gdraa_shard(N, r, L)
+                what = f"LL sgd N={N} {dt} mp={mixed} L={L} it{it} r{r}"
+                if mixed:
+                    compare(from_dev(mo_d[r]), model, "bf16", what=what + " model")
+                    compare(from_dev(w_d[r])[off:off + ln], w[off:off + ln], "f32",
+                            what=what + " master")
+                else:
+                    compare(from_dev(w_d[r]), w, "f32", what=what + " w")
+                compare(from_dev(v_d[r])[off:off + ln], v[off:off + ln], "f32",
+                        what=what + " v")
+                assert np.array_equal(from_dev(g_d[r]), gs[r]), what + " g changed"
+
+
+@pytest.mark.parametrize("N", [2, 4])
+def test_vr_mixed_call_sequence(N):
+    """Receive-slot parity alternates over every call of a rank, whichever kernel serves
+    it: interleave small means, small steps and two-shot steps on the same ranks."""
+    L_small, L_big = 10_001, 1_500_001
+    rng_calls = ["mean_s", "sgd_s", "sgd_b", "sgd_s", "mean_s", "mean_s", "sgd_s", "sgd_b",
+                 "sgd_s"]
+    w = {L: synth.w_like(31, L) for L in (L_small, L_big)}
+    v = {L: np.zeros(L, np.float32) for L in (L_small, L_big)}
+    w_d = {L: [to_dev(w[L]) for _ in range(N)] for L in w}
+    v_d = {L: [to_dev(v[L]) for _ in range(N)] for L in v}
+    for k, call in enumerate(rng_calls):
+        L = L_big if call.endswith("_b") else L_small
+        gs = make_grads("like", 40 + k, N, L, False)
+        g_d = [to_dev(g) for g in gs]
+        if call.startswith("mean"):
+            gdraa.gdraa_vr_allreduce_mean(g_d)
+            torch.cuda.synchronize()
+            exp = oracle.allreduce_mean(gs)
+            for r in range(N):
+                compare(from_dev(g_d[r]), exp, "f32", what=f"call {k} mean r{r}")
+            continue
+        w[L], v[L] = oracle.sgd_step(gs, w[L], v[L], 0.1, 0.9)
+        gdraa.gdraa_vr_sgd_step(w_d[L], g_d, v_d[L], 0.1, 0.9)
+        torch.cuda.synchronize()
+        for r in range(N):
+            off, ln = gdraa.gdraa_shard(N, r, L)
+            compare(from_dev(w_d[L][r]), w[L], "f32", what=f"call {k} {call} w r{r}")
+            compare(from_dev(v_d[L][r])[off:off + ln], v[L][off:off + ln], "f32",
+                    what=f"call {k} {call} v r{r}")
+
+
 @pytest.mark.parametrize("N,dt", [(2, "f32"), (4, "f32"), (8, "bf16")])
 def test_vr_chained_iterations(N, dt):
     """10 chained steps with fresh gradients each iteration (random family, P:246

@@ -92,10 +92,17 @@ def _worker(rank, world, sock, L_list, out_dir):
                 report["cases"] += 1
     st = gdraa.gdraa_get_stats()
     assert st["calls"] == calls, (st, calls)
-    # exactly two device synchronisations per call; small allreduce_mean calls take
-    # the latency path, whose synchronisation travels with the data (NEXT-2)
+    # exactly two device synchronisations per call; small calls take the latency
+    # paths, whose synchronisation travels with the data (NEXT-2)
     lim = gdraa.gdraa_small_message_bytes(world)
-    small = sum(2 for L in L_list for es in (4, 2) if L * es <= lim)   # 2 families each
+    small = 0
+    for L in L_list:
+        for es, code in ((4, gdraa.GDRAA_F32), (2, gdraa.GDRAA_BF16)):
+            step = L * es <= gdraa.gdraa_small_step_bytes(world, code)
+            step_mp = L * es <= gdraa.gdraa_small_step_bytes(world, code, mixed=True)
+            small += 2 * (L * es <= lim)                       # mean, both families
+            small += (1 + 3) * step                            # sgd: int 1 + like 3 steps
+            small += 2 * step_mp + 2 * step                    # mp and ex, both families
     assert st["ll_calls"] == small, (st, small)
     assert st["sync_waits"] == 2 * (calls - st["ll_calls"]), st
     report["stats"] = st

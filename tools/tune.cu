@@ -10,6 +10,7 @@
 //     lib : the library's launch shapes (LSU and TMA kernels)
 //     lsu : sweep of the LSU kernel's (U, threads, CTAs/SM)
 //     tma : sweep of the TMA kernel's (consumer warps, stages)
+//     tail: end-game variants of the TMA kernel (small-chunk size, in-flight depth)
 //     ctas: both kernels at grid caps 16/32/64/all (how many SMs the collective needs)
 #define GDRAA_TRACE 1
 #include "../paper_1802_02326_b200/csrc/gdraa_kernels.cu"
@@ -168,10 +169,10 @@ void lsu(int cap = 0) {
     run<TG, WORLD, MODE>(fn, THREADS, 0, (int)std::max<uint64_t>(gx, 1), "lsu", shape);
 }
 
-template <typename TG, int WORLD, int MODE, int CW, int ST>
+template <typename TG, int WORLD, int MODE, int CW, int ST, int TD = 4, int TDEP = ST, int ROT = 0>
 void tma(int cap = 0) {
-    using C = TmaCfg<TG, WORLD, MODE, CW, ST>;
-    auto fn = gdraa_tma_kernel<TG, WORLD, MODE, CW, ST>;
+    using C = TmaCfg<TG, WORLD, MODE, CW, ST, TD, TDEP, ROT>;
+    auto fn = gdraa_tma_kernel<TG, WORLD, MODE, CW, ST, TD, TDEP, ROT>;
     CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(fn),
                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     int per = 0;
@@ -182,7 +183,8 @@ void tma(int cap = 0) {
                                      (uint64_t)sm_count() * per);
     if (cap > 0) gx = std::min<uint64_t>(gx, cap);
     char shape[64];
-    std::snprintf(shape, sizeof shape, "CW%d_ST%d_CH%d_per%d", CW, ST, C::CH, per);
+    std::snprintf(shape, sizeof shape, "CW%d_ST%d_CH%d_TD%d_TDEP%d_ROT%d_per%d", CW, ST, C::CH,
+                  TD, C::TDEPTH, ROT, per);
     run<TG, WORLD, MODE>(fn, C::THREADS, C::SMEM, (int)std::max<uint64_t>(gx, 1), "tma", shape);
 }
 
@@ -206,6 +208,19 @@ void sweep() {
         tma<TG, WORLD, MODE, 8, 4>();
         tma<TG, WORLD, MODE, 8, 5>();
         tma<TG, WORLD, MODE, 16, 4>();
+    } else if (WHAT == "tail") {
+        // end-game variants of the library's TMA shape (16 consumer warps, 4 stages)
+        for (int rep = 0; rep < 2; ++rep) {
+            tma<TG, WORLD, MODE, 16, 4, 4, 4>();
+            tma<TG, WORLD, MODE, 16, 4, 8, 4>();
+            tma<TG, WORLD, MODE, 16, 4, 16, 4>();
+            tma<TG, WORLD, MODE, 16, 4, 4, 2>();
+            tma<TG, WORLD, MODE, 16, 4, 8, 2>();
+            tma<TG, WORLD, MODE, 16, 4, 16, 2>();
+            tma<TG, WORLD, MODE, 16, 4, 8, 1>();
+            tma<TG, WORLD, MODE, 16, 4, 4, 4, 1>();
+            tma<TG, WORLD, MODE, 16, 4, 8, 2, 1>();
+        }
     } else if (WHAT == "ctas") {
         for (int cap : {16, 32, 64, 0}) {
             lsu<TG, WORLD, MODE, S::U, S::THREADS, S::MINB>(cap);
@@ -227,7 +242,7 @@ void dispatch_world() {
 
 int main(int argc, char **argv) {
     if (argc < 5) {
-        std::fprintf(stderr, "usage: tune <world> <L> <f32|bf16> <sgd|mean> [iters] [lib|lsu|tma|ctas]\n");
+        std::fprintf(stderr, "usage: tune <world> <L> <f32|bf16> <sgd|mean> [iters] [lib|lsu|tma|tail|ctas]\n");
         return 1;
     }
     W = std::atoi(argv[1]);
