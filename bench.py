@@ -192,7 +192,7 @@ def run_reference(args):
         "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": float(np.mean(dts)) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": config_dict(args, L, g_dt, desc, N),
+        "data": "synthetic", "config": config_dict(args, L, g_dt, desc, N, "oracle (CPU)"),
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -202,14 +202,18 @@ def run_reference(args):
     return 0
 
 
-def config_dict(args, L, g_dt, desc, N):
+def config_dict(args, L, g_dt, desc, N, path=None):
     mp = args.config in MP_CONFIGS
+    s_g = 2 if g_dt == "bf16" else 4
     return {"workload": args.config, "description": desc, "L": L, "g_dtype": g_dt,
             "w_dtype": "f32 master sharded + bf16 model copy" if mp else "f32",
             "v_dtype": "f32", "lr": synth.PAPER_LR, "mom": synth.PAPER_MOM,
             "wd": PAPER_WD if mp else 0.0,
             "parallelism": f"dp{N}", "buffer_sets": args.sets,
-            "l2": f"inputs larger than L2: {args.sets} rotating (g, w, v) sets per rank"}
+            "l2": ("n/a: the CPU oracle on host memory" if args.sets <= 0 else
+                   f"inputs larger than L2: {args.sets} rotating (g, w, v) sets per rank "
+                   f"({args.sets * L * (s_g + 8 + (2 if mp else 0)) / 1e6:.0f} MB)"),
+            "path": path}
 
 
 # ---------------------------------------------------------------------------------------
@@ -222,7 +226,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="r50", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sets", type=int, default=3)
+    ap.add_argument("--sets", type=int, default=0,
+                    help="rotating (g, w, v) sets per rank; 0 = enough to exceed 2x L2")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
@@ -294,8 +299,17 @@ def main():
             return (self.model if mp else self.w)[off:off + ln]
 
     # synthetic inputs (host), then resident in HBM; S rotating sets so that no step
-    # finds its inputs in the 126 MB L2.
+    # finds its inputs in the 126 MB L2 (>= 3 sets, and >= 2x L2 of them in total).
+    if args.sets <= 0:
+        l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+        set_bytes = L * (s_g + 4 + 4 + (2 if mp else 0))
+        args.sets = max(3, -(-2 * l2 // set_bytes))
     sets = [StepSet(s) for s in range(args.sets)]
+    # which kernel serves the step (both give the same bits): N = 1 is a local fused
+    # SGD, small steps take the LL kernel (no device barrier), the rest the two-shot one
+    code = gdraa.GDRAA_BF16 if g_dt == "bf16" else gdraa.GDRAA_F32
+    path = ("local" if N == 1 else
+            "ll_sgd" if L * s_g <= gdraa.gdraa_small_step_bytes(N, code, mp) else "two_shot")
 
     def barrier():
         if world > 1:
@@ -434,7 +448,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": config_dict(args, L, g_dt, desc, N),
+            "config": config_dict(args, L, g_dt, desc, N, path),
             "value_definition": ("sum over ranks of per-rank algorithmic bytes / step time; "
                                  + (f"N=1: HBM bytes {per_rank / L:g}*L" if N == 1 else
                                     f"N>=2: NVLink bus bytes (N-1)/N*L*({s_g}+{s_w}) per rank")),

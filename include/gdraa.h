@@ -211,7 +211,7 @@ size_t gdraa_small_message_bytes(int world);
  * owner shard, g unchanged -- is bitwise the two-shot kernel's.
  *   world: 2..GDRAA_MAX_WORLD (0 otherwise); dtype: of g (GDRAA_F32 / GDRAA_BF16);
  *   mixed: nonzero for gdraa_sgd_step_mp (bf16 broadcast).
- * Default limit 2 MiB / (world - 1) (GDRAA_LL_SGD_MAX_BYTES overrides, 0 disables),
+ * Default limit 4 MiB / (world - 1) (GDRAA_LL_SGD_MAX_BYTES overrides, 0 disables),
  * lowered to what one sender's receive slot (gdraa_small_message_bytes) can hold.
  * Pure host function.
  */

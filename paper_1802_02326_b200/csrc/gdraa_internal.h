@@ -60,6 +60,7 @@ struct KParams {
     // [2 parities][world senders][ll_pairs] x uint4 {word0, flag, word1, flag}.
     uint4 *ll[kMaxWorld][kMaxWorld];
     uint64_t ll_pairs;                       // capacity in 8-byte payload pairs per sender
+    uint32_t ll_sleep_ns;                    // LL poll back-off cap (0 = spin)
     ErrBlock *err;                           // host-mapped (device alias)
     volatile uint64_t *done[kMaxWorld];      // host-mapped done flags (device alias) or null
     const volatile int32_t *abort;           // host-mapped job-server abort flag, or null:
@@ -111,6 +112,6 @@ uint64_t ll_sgd_limit_bytes(int world);
 // GDRAA_LL_MAX_BYTES overrides it (0 disables the LL path).
 uint64_t ll_limit_bytes(int world);
 constexpr uint64_t kLLBaseBytes = 4ull << 20;
-constexpr uint64_t kLLSgdBaseBytes = 2ull << 20;
+constexpr uint64_t kLLSgdBaseBytes = 4ull << 20;
 
 }  // namespace gdraa

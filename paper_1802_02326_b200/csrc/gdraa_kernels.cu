@@ -476,14 +476,22 @@ __device__ __forceinline__ uint4 ld_ll(const uint4 *p) {
 
 // Poll one LL entry until both flag words carry `flag`.  Bounded by timeout_ns; the
 // host-mapped abort flag is read only every 1024 polls (a read per poll from thousands
-// of polling threads would queue on PCIe and serialise the whole kernel).
+// of polling threads would queue on PCIe and serialise the whole kernel).  A thread whose
+// entry is not there yet backs off with __nanosleep (doubling up to max_sleep_ns; 0 = spin)
+// so that tens of thousands of waiting threads do not flood L2 with polls while the
+// peers' NVLink writes are trying to land there.
 __device__ __forceinline__ uint4 ll_wait(const uint4 *src, uint32_t flag, uint64_t timeout_ns,
-                                         const volatile int32_t *abort, bool &ok) {
+                                         const volatile int32_t *abort, uint32_t max_sleep_ns,
+                                         bool &ok) {
     uint4 r = ld_ll(src);
     if (r.y == flag && r.w == flag) return r;
     const uint64_t t0 = global_timer_ns();
-    uint32_t polls = 0;
+    uint32_t polls = 0, sleep_ns = 32;
     do {
+        if (max_sleep_ns != 0) {
+            __nanosleep(sleep_ns);
+            sleep_ns = sleep_ns * 2 > max_sleep_ns ? max_sleep_ns : sleep_ns * 2;
+        }
         r = ld_ll(src);
         if ((++polls & 1023u) == 0 &&
             (global_timer_ns() - t0 > timeout_ns || (abort != nullptr && *abort != 0))) {
@@ -576,7 +584,7 @@ gdraa_ll_kernel(const __grid_constant__ KParams p) {
                 continue;
             }
             const uint4 *src = p.ll[vr][rank] + (par * WORLD + q) * p.ll_pairs + j;
-            const uint4 r = ll_wait(src, flag, p.timeout_ns, p.abort, ok);
+            const uint4 r = ll_wait(src, flag, p.timeout_ns, p.abort, p.ll_sleep_ns, ok);
             if (!ok) {
                 report_timeout(p.err, 1, q, vr);
                 break;
@@ -660,7 +668,7 @@ gdraa_ll_sgd_kernel(const __grid_constant__ KParams p) {
     // poll one entry until it carries this call's flag (bounded; abandons on abort)
     bool ok = true;
     auto poll = [&](const uint4 *src, int q, int phase) -> uint2 {
-        const uint4 r = ll_wait(src, flag, p.timeout_ns, p.abort, ok);
+        const uint4 r = ll_wait(src, flag, p.timeout_ns, p.abort, p.ll_sleep_ns, ok);
         if (!ok) report_timeout(p.err, phase, q, vr);
         return make_uint2(r.x, r.z);
     };

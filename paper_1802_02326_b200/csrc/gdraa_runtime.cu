@@ -335,6 +335,7 @@ void fill_common(KParams &p, uint64_t n) {
         p.ll[0][q] = g.peer_ll[q];
     }
     p.ll_pairs = g.ll_pairs;
+    p.ll_sleep_ns = static_cast<uint32_t>(env_u64("GDRAA_LL_SLEEP_NS", 256));
     p.err = g.err_d;
     p.done[0] = g.done_d;
     p.abort = g.abort_d;
@@ -497,6 +498,7 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
     }
     p.err = d->err_d;
     p.ll_pairs = d->ll[world] != nullptr ? d->ll_pairs[world] : 0;
+    p.ll_sleep_ns = static_cast<uint32_t>(env_u64("GDRAA_LL_SLEEP_NS", 256));
     const size_t es = dtype == GDRAA_F32 ? 4 : 2;
     if (mode == kMean && world > 1 && n * es <= 8 * p.ll_pairs) {   // latency path
         cudaError_t e = launch_gdraa_ll(p, dtype, world, true, s);

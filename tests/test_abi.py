@@ -108,7 +108,7 @@ def test_small_message_threshold():
 
 @pytest.mark.parametrize("mixed", [False, True])
 def test_small_step_threshold(mixed):
-    """Small-message SGD threshold: at most 2 MiB / (N-1) of gradient bytes, and the
+    """Small-message SGD threshold: at most 4 MiB / (N-1) of gradient bytes, and the
     largest n whose padded shard (gradient + broadcast part) fits one sender's slot."""
     assert gdraa.gdraa_small_step_bytes(1) == 0 and gdraa.gdraa_small_step_bytes(9) == 0
     for N in range(2, 9):
@@ -116,7 +116,7 @@ def test_small_step_threshold(mixed):
         for code, sg in ((gdraa.GDRAA_F32, 4), (gdraa.GDRAA_BF16, 2)):
             sw = 2 if mixed else 4
             lim = gdraa.gdraa_small_step_bytes(N, code, mixed)
-            assert 0 < lim <= (2 << 20) // (N - 1) and lim % sg == 0
+            assert 0 < lim <= (4 << 20) // (N - 1) and lim % sg == 0
 
             def fits(n):
                 blk = oracle.partition(n, N, 0, Q=64)[1]
@@ -124,4 +124,4 @@ def test_small_step_threshold(mixed):
 
             n = lim // sg
             assert fits(n)
-            assert n == (2 << 20) // (N - 1) // sg or not fits(n + 1)
+            assert n == (4 << 20) // (N - 1) // sg or not fits(n + 1)

@@ -48,19 +48,20 @@ __device__ __forceinline__ uint64_t ld_acq(const uint64_t *p) {
     return v;
 }
 
+// The library's scheme: thread q (q != rank) stores into peer q's slot and polls our slot q,
+// in parallel, then the CTA synchronises.
 __global__ void unicast_rounds(uint64_t *const *peer_slots, uint64_t *mine, int rank, int n,
                                int rounds) {
-    if (threadIdx.x != 0) return;
+    const int q = threadIdx.x;
     for (uint64_t e = 1; e <= static_cast<uint64_t>(rounds); ++e) {
-        for (int q = 0; q < n; ++q)
-            if (q != rank)
-                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer_slots[q] + rank),
-                             "l"(e)
-                             : "memory");
-        for (int q = 0; q < n; ++q)
-            if (q != rank)
-                while (ld_acq(mine + q) < e) {
-                }
+        if (q < n && q != rank) {
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer_slots[q] + rank),
+                         "l"(e)
+                         : "memory");
+            while (ld_acq(mine + q) < e) {
+            }
+        }
+        __syncthreads();
     }
 }
 
