@@ -18,7 +18,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.multigpu,
                                  reason="needs >= 2 GPUs")]
 
 
-def _setup(rank, world, sock, timeout_ms):
+def _setup(rank, world, sock, timeout_ms, n):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     os.environ["GDRAA_JOBSERVER"] = sock
@@ -27,18 +27,18 @@ def _setup(rank, world, sock, timeout_ms):
     from paper_1802_02326_b200 import gdraa
     gdraa.gdraa_init(world, rank)
     dev = f"cuda:{rank}"
-    w = torch.zeros(1 << 20, device=dev)
-    g = torch.ones(1 << 20, device=dev)
-    v = torch.zeros(1 << 20, device=dev)
+    w = torch.zeros(n, device=dev)
+    g = torch.ones(n, device=dev)
+    v = torch.zeros(n, device=dev)
     gdraa.gdraa_register(w)
     gdraa.gdraa_register(g)
     return gdraa, w, g, v
 
 
-def _timeout_worker(rank, world, sock, out, mode):
+def _timeout_worker(rank, world, sock, out, mode, n):
     # rank 0 gives up after 1.5 s when the peer just skips the call; when the peer dies
     # it keeps a 60 s timeout, so only the job server's abort flag can end its wait early
-    gdraa, w, g, v = _setup(rank, world, sock, 1500 if rank == 0 and mode == "skip" else 60000)
+    gdraa, w, g, v = _setup(rank, world, sock, 1500 if rank == 0 and mode == "skip" else 60000, n)
     res = {"rank": rank}
     if rank == 0:
         t0 = time.time()
@@ -67,13 +67,13 @@ def _timeout_worker(rank, world, sock, out, mode):
         json.dump(res, f)
 
 
-def _run(tmp_path, mode):
+def _run(tmp_path, mode, n):
     from paper_1802_02326_b200 import jobserver
     world = 2
     sock = str(tmp_path / "js.sock")
     js = jobserver.start(world, sock)
     ctx = mp.get_context("spawn")
-    procs = [ctx.Process(target=_timeout_worker, args=(r, world, sock, str(tmp_path), mode))
+    procs = [ctx.Process(target=_timeout_worker, args=(r, world, sock, str(tmp_path), mode, n))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -83,17 +83,24 @@ def _run(tmp_path, mode):
     return [p.exitcode for p in procs], json.load(open(tmp_path / "r0.json")), out
 
 
-def test_peer_timeout_names_missing_rank(tmp_path):
-    codes, r0, _ = _run(tmp_path, "skip")
+# 2^18 fp32 elements take the small-message SGD kernel (data-carried synchronisation),
+# 2^21 the two-shot kernel (device barriers): both must time out and abort the same way
+SIZES = [1 << 18, 1 << 21]
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_peer_timeout_names_missing_rank(tmp_path, n):
+    codes, r0, _ = _run(tmp_path, "skip", n)
     assert codes == [0, 0], codes
     assert 1.0 < r0["kernel_s"] < 20, r0
     assert r0["second"] == "GDRAA_ETIMEOUT" and "missing rank(s) 1" in r0["msg"], r0
     assert r0["finalize"] == "GDRAA_ETIMEOUT", r0
 
 
-def test_dead_rank_aborts_the_wait(tmp_path):
+@pytest.mark.parametrize("n", SIZES)
+def test_dead_rank_aborts_the_wait(tmp_path, n):
     # rank 0's kernel would wait 60 s; the job server's abort flag ends it in seconds
-    codes, r0, js_out = _run(tmp_path, "die")
+    codes, r0, js_out = _run(tmp_path, "die", n)
     assert codes[1] == 3 and codes[0] == 0, codes
     assert r0["kernel_s"] < 15, r0
     assert r0["second"] == "GDRAA_EJOBSERVER" and "rank 1" in r0["msg"], r0

@@ -414,5 +414,44 @@ int main(int argc, char **argv) {
     run_bidir("memcpy_peer", bytes, [&](int d, cudaStream_t s) {
         CK(cudaMemcpyPeerAsync(p.buf[1 - d][2], 1 - d, p.buf[d][0], d, bytes, s));
     });
+    // Hybrid: can copy engines carry part of the traffic while SMs carry the rest, and
+    // does the mix beat the SM-only ceiling?  Each device moves `bytes` per direction in
+    // total: a fraction f by SM kernel (pull or push) on stream s, the rest by a
+    // copy-engine push on a side stream, concurrently.
+    {
+        cudaStream_t side[2];
+        cudaEvent_t fork[2], join[2];
+        for (int d = 0; d < 2; ++d) {
+            CK(cudaSetDevice(d));
+            CK(cudaStreamCreateWithFlags(&side[d], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&fork[d], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&join[d], cudaEventDisableTiming));
+        }
+        for (int pct : {25, 50, 75}) {
+            const size_t sm_b = bytes / 100 * pct / 256 * 256, ce_b = bytes - sm_b;
+            for (int kind = 0; kind < 2; ++kind) {   // 0: SM pull, 1: SM push
+                for (int grid : {32, 0}) {
+                    char name[96];
+                    std::snprintf(name, sizeof name, "hybrid_sm%s%d_ctas%s_ce_push%d",
+                                  kind ? "push" : "pull", pct, grid ? "032" : "all", 100 - pct);
+                    run_bidir(name, bytes, [&](int d, cudaStream_t s) {
+                        CK(cudaEventRecord(fork[d], s));
+                        CK(cudaStreamWaitEvent(side[d], fork[d], 0));
+                        CK(cudaMemcpyPeerAsync(p.buf[1 - d][2] + sm_b, 1 - d, p.buf[d][0] + sm_b, d,
+                                               ce_b, side[d]));
+                        const int gx = grid ? grid : g_sms;
+                        if (kind == 0)
+                            copy_kernel<4><<<gx, 1024, 0, s>>>((const uint4 *)p.buf[1 - d][0],
+                                                               (uint4 *)p.buf[d][1], sm_b / 16);
+                        else
+                            copy_kernel<4><<<gx, 1024, 0, s>>>((const uint4 *)p.buf[d][0],
+                                                               (uint4 *)p.buf[1 - d][1], sm_b / 16);
+                        CK(cudaEventRecord(join[d], side[d]));
+                        CK(cudaStreamWaitEvent(s, join[d], 0));
+                    });
+                }
+            }
+        }
+    }
     return 0;
 }
