@@ -247,3 +247,125 @@ def test_multiprocess_least_squares_ssgd(tmp_path):
     reps = [json.load(open(tmp_path / f"ls{r}.json")) for r in range(world)]
     assert all(r["gap"] < 1e-5 for r in reps), [r["gap"] for r in reps]
     assert all(r["w"] == reps[0]["w"] for r in reps)      # bitwise identical replicas
+
+
+# ---------------------------------------------------------------------------------------
+# Full BASELINE sizes in bench.py's launch configuration (one process per GPU, the public
+# calls, the two-shot kernel), compared with the oracle on sampled windows: the oracle is
+# elementwise, so a window of every rank's gradient (regenerated from synth's
+# counter-based streams) and of w/v reproduces the exact expected bits there.
+# ---------------------------------------------------------------------------------------
+FULL = [("r50", "f32", False), ("r101", "f32", False), ("r50", "bf16", False),
+        ("r50", "bf16", True)]
+WIN = 4096
+
+
+def _windows(L, world, seed):
+    import synth
+    from paper_1802_02326_b200 import gdraa
+    starts = {0, L - WIN, synth.neg_zero_segment(seed, L) * synth.SEGMENT}
+    for r in range(1, world):                      # every shard boundary
+        off, _ = gdraa.gdraa_shard(world, r, L)
+        starts.add(max(0, off - WIN // 2))
+    rng = np.random.default_rng(seed)
+    starts.update(int(x) for x in rng.integers(0, L - WIN, 8))
+    return sorted(min(max(0, s), L - WIN) for s in starts)
+
+
+def _window_grads(seed, world, a, L, bf16):
+    import synth
+    k = synth.neg_zero_segment(seed, L) * synth.SEGMENT
+    out = []
+    for p in range(world):
+        g = synth.grad_like(seed, p, WIN, start=a)
+        lo, hi = max(a, k), min(a + WIN, k + synth.SEGMENT)   # the all-ranks -0.0 segment
+        if lo < hi:
+            g[lo - a:hi - a] = np.float32(-0.0)
+        out.append(synth.to_bf16_bits_trunc(g) if bf16 else g)
+    return out
+
+
+def _full_worker(rank, world, sock, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    import synth
+    from paper_1802_02326_b200 import gdraa
+    from tests._parity import compare
+    from tests.test_gpu_parity import from_dev, to_dev
+
+    torch.cuda.set_device(rank)
+    dev = f"cuda:{rank}"
+    os.environ["GDRAA_JOBSERVER"] = sock
+    gdraa.gdraa_init(world, rank)
+    lr, mom, wd = synth.PAPER_LR, synth.PAPER_MOM, 0.001
+    checked = 0
+    for name, dt, mp_ in FULL:
+        L = synth.L_R50 if name == "r50" else synth.L_R101
+        bf16 = dt == "bf16"
+        assert L * (2 if bf16 else 4) > gdraa.gdraa_small_step_bytes(world)   # two-shot
+        off, ln = gdraa.gdraa_shard(world, rank, L)
+        w0 = synth.w_like(3, L)
+        w = to_dev(w0, dev=dev)
+        v = torch.zeros(L, device=dev)
+        model = torch.zeros(L, dtype=torch.bfloat16, device=dev) if mp_ else None
+        gdraa.gdraa_register(model if mp_ else w)
+        wins = _windows(L, world, 40)
+        state = {a: (w0[a:a + WIN].copy(), np.zeros(WIN, np.float32)) for a in wins}
+        for it in range(2):                                # two chained steps
+            seed = 40 + it
+            gh = synth.grad_like_full(seed, rank, L)
+            g = to_dev(synth.to_bf16_bits_trunc(gh) if bf16 else gh, bf16, dev)
+            del gh
+            gdraa.gdraa_register(g)
+            if mp_:
+                gdraa.gdraa_sgd_step_mp(w, model, g, v, lr, mom, wd)
+            else:
+                gdraa.gdraa_sgd_step(w, g, v, lr, mom)
+            torch.cuda.synchronize()
+            wh, vh = from_dev(w), from_dev(v)
+            mh = from_dev(model) if mp_ else None
+            for a in wins:
+                gs = _window_grads(seed, world, a, L, bf16)
+                if mp_:
+                    we, ve, me = oracle.sgd_step_wd(gs, *state[a], lr, mom, wd,
+                                                    model_dtype=oracle.BF16)
+                    compare(mh[a:a + WIN], me, "bf16", what=f"{name} mp model it{it} @{a} r{rank}")
+                else:
+                    we, ve = oracle.sgd_step(gs, *state[a], lr, mom)
+                    compare(wh[a:a + WIN], we, "f32", what=f"{name} {dt} w it{it} @{a} r{rank}")
+                # owner-sharded state (v, and the fp32 master for _mp): owned indices only
+                lo, hi = max(a, off), min(a + WIN, off + ln)
+                if lo < hi:
+                    compare(vh[lo:hi], ve[lo - a:hi - a], "f32", what=f"{name} v @{a} r{rank}")
+                    if mp_:
+                        compare(wh[lo:hi], we[lo - a:hi - a], "f32", what=f"{name} master r{rank}")
+                state[a] = (we, ve)
+                checked += WIN
+            gdraa.gdraa_deregister(g)
+            del g
+        gdraa.gdraa_deregister(model if mp_ else w)
+        del w, v, model
+        torch.cuda.empty_cache()
+    st = gdraa.gdraa_get_stats()
+    assert st["ll_calls"] == 0 and st["sync_waits"] == 2 * st["calls"], st
+    gdraa.gdraa_finalize()
+    with open(os.path.join(out_dir, f"full{rank}.json"), "w") as f:
+        json.dump({"checked": checked}, f)
+
+
+def test_multiprocess_full_size_sampled(tmp_path):
+    """Configs 2, 3, 4 (+ NEXT-1) at full size through the multi-process path, two chained
+    steps, bit-exact on windows at every shard boundary, the ragged end, the all-ranks
+    -0.0 segment (AMB-3) and random places."""
+    from paper_1802_02326_b200 import jobserver
+    world = min(torch.cuda.device_count(), 8)
+    sock = str(tmp_path / "js.sock")
+    js = jobserver.start(world, sock)
+    try:
+        mp.start_processes(_full_worker, args=(world, sock, str(tmp_path)), nprocs=world,
+                           join=True, start_method="spawn")
+    finally:
+        js.communicate(timeout=120)
+    for r in range(world):
+        assert json.load(open(tmp_path / f"full{r}.json"))["checked"] > 0
