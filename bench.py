@@ -157,6 +157,28 @@ class OracleSample:
                                                   synth.PAPER_MOM)
         return time.perf_counter() - t0
 
+    def step_mt(self, pool, k):
+        """The same oracle call on k contiguous pieces of the sample, one per thread
+        (ctypes drops the GIL; the pieces are independent, so the result is identical)."""
+        cuts = [self.n * i // k for i in range(k + 1)]
+
+        def piece(i):
+            a, b = cuts[i], cuts[i + 1]
+            gs = [g[a:b] for g in self.gs]
+            if self.mp:
+                w, v, _ = self.oracle.sgd_step_wd(gs, self.w[a:b], self.v[a:b], synth.PAPER_LR,
+                                                  synth.PAPER_MOM, PAPER_WD,
+                                                  model_dtype=self.oracle.BF16)
+            else:
+                w, v = self.oracle.sgd_step(gs, self.w[a:b], self.v[a:b], synth.PAPER_LR,
+                                            synth.PAPER_MOM)
+            return a, b, w, v
+
+        t0 = time.perf_counter()
+        for a, b, w, v in pool.map(piece, range(k)):
+            self.w[a:b], self.v[a:b] = w, v
+        return time.perf_counter() - t0
+
     def describe(self, reps):
         return (f"{reps} oracle sgd_step calls over the first {self.n} elements of each of "
                 f"the {self.N} rank buffers (L={self.L}); single thread")
@@ -171,6 +193,20 @@ def oracle_baseline(L, N, g_dt, budget_s, mp=False):
         total += s.step()
         reps += 1
     return s.bytes / (total / reps), s.describe(reps), total / reps
+
+
+def oracle_baseline_mt(L, N, g_dt, budget_s, mp=False):
+    """The labelled k-thread variant: k = host cores, same sample."""
+    from concurrent.futures import ThreadPoolExecutor
+    k = os.cpu_count() or 1
+    s = OracleSample(L, N, g_dt, mp, n=1 << 23)    # 8M elements: enough work per thread
+    with ThreadPoolExecutor(max_workers=k) as pool:
+        s.step_mt(pool, k)
+        reps, total = 0, 0.0
+        while total < budget_s:
+            total += s.step_mt(pool, k)
+            reps += 1
+    return s.bytes / (total / reps), k, reps, s.n
 
 
 def run_reference(args):
@@ -443,6 +479,12 @@ def main():
             cv, sample, _ = oracle_baseline(L, N, g_dt, 10.0, mp)
             cpu = {"value": cv / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
                    "sample": sample}
+            mv, k, mreps, mn = oracle_baseline_mt(L, N, g_dt, 5.0, mp)
+            cpu["threaded_variant"] = {
+                "value": mv / 1e9, "unit": "GB/s", "cores": k,
+                "note": f"same oracle on the first {mn} elements of each rank buffer, split "
+                        f"into {k} contiguous pieces on {k} threads ({mreps} steps); a "
+                        f"labelled variant, not the baseline"}
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
