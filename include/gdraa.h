@@ -69,8 +69,12 @@ typedef enum {
  * Uses the CUDA device current on the calling thread.  For world > 1 the job server
  * socket path is read from the environment variable GDRAA_JOBSERVER (started by
  * paper_1802_02326_b200.jobserver); the call blocks until all ranks have joined and the
- * signal pads are mapped (GDRAA_CONNECT_TIMEOUT_MS, default 120000).
- * Errors: EINVAL (range), ESTATE (already initialised), EJOBSERVER, ECUDA.
+ * signal pads are mapped (GDRAA_CONNECT_TIMEOUT_MS, default 120000).  The small-message
+ * thresholds (GDRAA_LL_MAX_BYTES, GDRAA_LL_SGD_MAX_BYTES) are read here, fixed for the
+ * communicator's lifetime and checked to agree on every rank, since they decide which
+ * kernel -- with which synchronisation protocol -- serves a call.
+ * Errors: EINVAL (range), ESTATE (already initialised), ESHAPE (ranks disagree on the
+ * thresholds), EJOBSERVER, ECUDA.
  */
 int gdraa_init(int world, int rank);
 
@@ -211,9 +215,9 @@ size_t gdraa_small_message_bytes(int world);
  * owner shard, g unchanged -- is bitwise the two-shot kernel's.
  *   world: 2..GDRAA_MAX_WORLD (0 otherwise); dtype: of g (GDRAA_F32 / GDRAA_BF16);
  *   mixed: nonzero for gdraa_sgd_step_mp (bf16 broadcast).
- * Default limit 4 MiB / (world - 1) (GDRAA_LL_SGD_MAX_BYTES overrides, 0 disables),
- * lowered to what one sender's receive slot (gdraa_small_message_bytes) can hold.
- * Pure host function.
+ * Default limit 4 MiB / (world - 1) (GDRAA_LL_SGD_MAX_BYTES overrides, 0 disables; a
+ * communicator reads it once, at gdraa_init), lowered to what one sender's receive slot
+ * (gdraa_small_message_bytes) can hold.  Pure host function (reads the environment).
  */
 size_t gdraa_small_step_bytes(int world, int dtype, int mixed);
 

@@ -138,6 +138,7 @@ struct State {
     uint4 *ll = nullptr;                // small-message receive slots (world > 1)
     uint4 *peer_ll[kMaxWorld] = {};
     uint64_t ll_pairs = 0;
+    uint64_t ll_sgd_limit = 0;          // small-message SGD threshold (bytes), fixed at init
     ErrBlock *err_h = nullptr, *err_d = nullptr;
     volatile uint64_t *done_d = nullptr;
     const volatile int32_t *abort_d = nullptr;   // device alias of the page's abort flag
@@ -666,6 +667,23 @@ int gdraa_init(int world, int rank) {
         if (rc) return cleanup_fail(rc);
         for (int p = 0; p < world; ++p) g.peer_ll[p] = static_cast<uint4 *>(lpeers[p]);
     }
+    // Path selection must agree on every rank (a rank on the LL path and a peer on the
+    // two-shot path would wait for each other until the timeout): the thresholds are fixed
+    // here and checked across ranks through the job server (registration sequence 3).
+    g.ll_sgd_limit = g.ll_pairs ? ll_sgd_limit_bytes(world) : 0;
+    if (world > 1) {
+        proto::Reg cfg{};
+        cfg.what = 3;
+        cfg.n = g.ll_sgd_limit;
+        cfg.dtype = static_cast<int32_t>(std::min<uint64_t>(g.ll_pairs, INT32_MAX));
+        proto::RegOk all{};
+        int rc = exchange(cfg, &all);
+        if (rc == GDRAA_ESHAPE)
+            rc = fail(GDRAA_ESHAPE, "ranks disagree on the small-message thresholds "
+                      "(GDRAA_LL_MAX_BYTES / GDRAA_LL_SGD_MAX_BYTES must match on every rank): %s",
+                      t_err.c_str());
+        if (rc) return cleanup_fail(rc);
+    }
     g.inited = true;
     return GDRAA_OK;
 }
@@ -806,7 +824,7 @@ static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, 
     }
     p.v[0] = static_cast<float *>(offset_ptr(v, first, 4));
     p.wm[0] = mode == kSgdMp ? static_cast<float *>(offset_ptr(wm, first, 4)) : nullptr;
-    if (g.ll != nullptr && count * eg <= ll_sgd_limit_bytes(g.world) &&
+    if (g.ll != nullptr && count * eg <= g.ll_sgd_limit &&
         ll_sgd_fits(p.blk, rg->dtype, mode, g.ll_pairs)) {
         // small message: the data carries both synchronisations (same result, bit for bit)
         cudaError_t e = launch_gdraa_ll_sgd(p, rg->dtype, mode, 1, false,

@@ -105,3 +105,44 @@ def test_dead_rank_aborts_the_wait(tmp_path, n):
     assert r0["kernel_s"] < 15, r0
     assert r0["second"] == "GDRAA_EJOBSERVER" and "rank 1" in r0["msg"], r0
     assert "disconnected" in js_out
+
+
+def _mismatch_worker(rank, world, sock, out):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["GDRAA_JOBSERVER"] = sock
+    # rank 1 would serve small steps with the two-shot kernel, rank 0 with the LL kernel
+    os.environ["GDRAA_LL_SGD_MAX_BYTES"] = "0" if rank == 1 else str(1 << 20)
+    torch.cuda.set_device(rank)
+    from paper_1802_02326_b200 import gdraa
+    res = {"rank": rank}
+    try:
+        gdraa.gdraa_init(world, rank)
+        res["init"] = "ok"
+        gdraa.gdraa_finalize()
+    except gdraa.GdraaError as e:
+        res["init"] = e.name
+        res["msg"] = str(e)
+    with open(os.path.join(out, f"m{rank}.json"), "w") as f:
+        json.dump(res, f)
+
+
+def test_threshold_mismatch_rejected_at_init(tmp_path):
+    """Ranks that would pick different kernels for the same call are refused at
+    gdraa_init (GDRAA_ESHAPE on every rank) instead of timing out mid-training."""
+    from paper_1802_02326_b200 import jobserver
+    world = 2
+    sock = str(tmp_path / "js.sock")
+    js = jobserver.start(world, sock)
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_mismatch_worker, args=(r, world, sock, str(tmp_path)))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    js.communicate(timeout=60)
+    for r in range(world):
+        res = json.load(open(tmp_path / f"m{r}.json"))
+        assert res["init"] == "GDRAA_ESHAPE", res
+        assert "GDRAA_LL_SGD_MAX_BYTES" in res["msg"], res
