@@ -1172,6 +1172,18 @@ TmaLaunch pick_tma_t(int mode, int world) {
     }
 }
 
+// Grid sizing for shards smaller than a full wave: one CTA per end-game (small) chunk, so
+// a mid-size call spreads over every SM instead of one CTA per big chunk (a CTA moves
+// only ~5 GB/s over NVLink, so few CTAs make a mid-size call latency-bound).
+// GDRAA_GRID_SMALL=0 sizes by big chunks (the earlier rule; A/B measurements only).
+bool grid_by_small_chunks() {
+    static const bool v = [] {
+        const char *e = std::getenv("GDRAA_GRID_SMALL");
+        return e == nullptr || e[0] != '0';
+    }();
+    return v;
+}
+
 int env_max_ctas() {
     static const int v = [] {
         const char *e = std::getenv("GDRAA_MAX_CTAS");
@@ -1273,7 +1285,8 @@ cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows, boo
     if (env_cap > 0 && env_cap < cap) cap = env_cap;
     if (cap < 1) return cudaErrorInvalidConfiguration;
     const uint64_t nvec = (p.blk + E - 1) / E;
-    const uint64_t per_chunk = static_cast<uint64_t>(l.threads) * l.u;
+    const uint64_t per_chunk =
+        static_cast<uint64_t>(l.threads) * (grid_by_small_chunks() ? 1 : l.u);
     const uint64_t want = (nvec + per_chunk - 1) / per_chunk;   // chunks of the largest shard
     int gx = static_cast<int>(want < static_cast<uint64_t>(cap) ? want : cap);
     if (gx < 1) gx = 1;
@@ -1418,7 +1431,8 @@ cudaError_t launch_gdraa_tma(const KParams &p, int dtype, int mode, int vr_rows,
     const int env_cap = env_max_ctas();
     if (env_cap > 0 && env_cap < cap) cap = env_cap;
     if (cap < 1) return cudaErrorInvalidConfiguration;
-    const uint64_t want = ((p.blk & ~7ull) + l.ch - 1) / l.ch;   // chunks of the largest shard
+    const uint64_t ch = grid_by_small_chunks() ? l.ch / 4 : l.ch;   // end-game chunk: CH/4
+    const uint64_t want = ((p.blk & ~7ull) + ch - 1) / ch;   // chunks of the largest shard
     int gx = static_cast<int>(want < static_cast<uint64_t>(cap) ? want : cap);
     if (gx < 1) gx = 1;
     if (grid_x_out) *grid_x_out = gx;
