@@ -127,6 +127,50 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+class NvlinkCounters:
+    """Measured NVLink bytes of this GPU (all links, each direction) from NVML's per-link
+    counters: NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / RCV_BYTES (fields 202 / 204), else
+    THROUGHPUT_DATA_TX / RX (138 / 139, KiB).  Read around an untimed pass of steps; the
+    per-step difference is the N >= 2 analogue of ncu's dram traffic (ncu cannot replay a
+    kernel that waits on other GPUs).  tools/nvlink_counters.py calibrates the families
+    against a known peer copy (profiles/r36_nvlink_counters_calibration.jsonl)."""
+
+    FAMILIES = (("NVML_FI_DEV_NVLINK_COUNT_{XMIT,RCV}_BYTES", 202, 204, 1),
+                ("NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_{TX,RX}", 138, 139, 1024))
+
+    def __init__(self, sampler):
+        self.ok, self.family = False, None
+        if sampler is None or not sampler.ok:
+            return
+        self.nv, self.h = sampler.nv, sampler.h
+        try:
+            v = self.nv.nvmlDeviceGetFieldValues(self.h, [91])[0]   # NVLINK_LINK_COUNT
+            self.links = int(v.value.uiVal) if v.nvmlReturn == 0 else 18
+        except Exception:   # noqa: BLE001
+            self.links = 18
+        for fam in self.FAMILIES:
+            if self._read(fam) is not None:
+                self.family, self.ok = fam, True
+                break
+
+    def _read(self, fam):
+        _, tx, rx, scale = fam
+        ids = [(tx, l) for l in range(self.links)] + [(rx, l) for l in range(self.links)]
+        try:
+            vals = self.nv.nvmlDeviceGetFieldValues(self.h, ids)
+        except Exception:   # noqa: BLE001
+            return None
+        good = [v.nvmlReturn == 0 for v in vals]
+        if not any(good):
+            return None
+        t = sum(int(v.value.ullVal) for v, g in zip(vals[:self.links], good) if g)
+        r = sum(int(v.value.ullVal) for v, g in zip(vals[self.links:], good[self.links:]) if g)
+        return t * scale, r * scale
+
+    def read(self):
+        return self._read(self.family) if self.ok else None
+
+
 # ---------------------------------------------------------------------------------------
 # the oracle as a CPU baseline (rank 0 only)
 # ---------------------------------------------------------------------------------------
@@ -249,7 +293,9 @@ def config_dict(args, L, g_dt, desc, N, path=None):
             "l2": ("n/a: the CPU oracle on host memory" if args.sets <= 0 else
                    f"inputs larger than L2: {args.sets} rotating (g, w, v) sets per rank "
                    f"({args.sets * L * (s_g + 8 + (2 if mp else 0)) / 1e6:.0f} MB)"),
-            "path": path}
+            "path": path,
+            "timing": ("one CUDA-graph replay of the K steps" if getattr(args, "graph", False)
+                       else "eager Python loop of the K steps")}
 
 
 # ---------------------------------------------------------------------------------------
@@ -267,6 +313,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-nvlink-counters", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="time one CUDA-graph replay of the K steps instead of an eager loop")
     args = ap.parse_args()
     # Exactly one JSON line on stdout: anything libraries print (NCCL banners, ...) goes
     # to stderr; the result line goes to the saved stdout.
@@ -324,11 +373,12 @@ def main():
                 gdraa.gdraa_register(self.w)
             gdraa.gdraa_register(self.g)
 
-        def step(self):
+        def step(self, s=None):
+            s = stream if s is None else s
             if mp:
-                gdraa.gdraa_sgd_step_mp(self.w, self.model, self.g, self.v, lr, mom, wd, stream)
+                gdraa.gdraa_sgd_step_mp(self.w, self.model, self.g, self.v, lr, mom, wd, s)
             else:
-                gdraa.gdraa_sgd_step(self.w, self.g, self.v, lr, mom, stream)
+                gdraa.gdraa_sgd_step(self.w, self.g, self.v, lr, mom, s)
 
         def result_shard(self):
             """This rank's share of the step's result (read back by the e2e leg)."""
@@ -356,6 +406,20 @@ def main():
         sets[k % len(sets)].step()
     barrier()
 
+    graph = None
+    if args.graph:
+        # the K timed steps captured once into a CUDA graph (host launch cost out of the
+        # step time; the library's epochs live in device memory, so replays are valid)
+        cap = torch.cuda.Stream()
+        g0 = gdraa.gdraa_get_stats()["launches"]
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            for k in range(args.steps):
+                sets[k % len(sets)].step(cap)
+        graph_launches = gdraa.gdraa_get_stats()["launches"] - g0
+        graph.replay()   # untimed warm-up replay
+        barrier()
+
     st0 = gdraa.gdraa_get_stats()
     clocks = ClockSampler(local) if rank == 0 else None
     barrier()
@@ -363,8 +427,11 @@ def main():
         clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for k in range(args.steps):
-        sets[k % len(sets)].step()
+    if graph is not None:
+        graph.replay()
+    else:
+        for k in range(args.steps):
+            sets[k % len(sets)].step()
     ev1.record(stream)
     torch.cuda.synchronize()
     if clocks:
@@ -377,7 +444,31 @@ def main():
     barrier()
     st1 = gdraa.gdraa_get_stats()
     launches = st1["launches"] - st0["launches"]
+    if graph is not None:   # replays do not pass through the host launch counter
+        launches = graph_launches
     ms_step = ms / args.steps
+
+    # ---- measured NVLink bytes per step (untimed pass, rank 0's counters) ----
+    nvl = None
+    if world > 1 and not args.no_nvlink_counters:
+        ctr = NvlinkCounters(clocks) if rank == 0 else None
+        barrier()
+        if ctr is not None and ctr.ok:
+            time.sleep(1.0)   # let the counters settle
+            c0 = ctr.read()
+        barrier()
+        for k in range(args.steps):
+            sets[k % len(sets)].step()
+        barrier()
+        if ctr is not None and ctr.ok:
+            time.sleep(1.5)
+            c1 = ctr.read()
+            if c0 is not None and c1 is not None:
+                nvl = {"tx_bytes_per_launch": (c1[0] - c0[0]) / args.steps,
+                       "rx_bytes_per_launch": (c1[1] - c0[1]) / args.steps,
+                       "source": f"NVML {ctr.family[0]} summed over {ctr.links} links, "
+                                 f"rank 0, {args.steps} untimed steps"}
+        barrier()
     per_rank = algorithmic_bytes(L, N, s_g, s_w)
     value = per_rank * N / (ms_step * 1e-3) / 1e9           # whole job
     achieved = per_rank / (ms_step * 1e-3) / 1e9            # per rank = per launch
@@ -473,6 +564,10 @@ def main():
                     "frac_of_nominal_900": achieved / NVLINK_NOMINAL_GBS,
                     "bytes_per_launch": per_rank}
         roof["traffic"] = ncu_traffic(args.config, N)
+        if nvl is not None:   # N >= 2: the bound resource's measured bytes per launch
+            nvl["algorithmic_bytes_per_launch"] = per_rank
+            nvl["rx_over_algorithmic"] = nvl["rx_bytes_per_launch"] / per_rank
+            roof["nvlink_traffic"] = nvl
         roof["kernel_ms"] = ms_step
         cpu = None
         if N == 1 and not args.no_cpu_baseline:

@@ -91,6 +91,12 @@ def _ptr(x):
         return None
     if isinstance(x, int):
         return x
+    # the library sees only the pointer: a host or strided tensor would be read as if it
+    # were a dense device buffer, so refuse it here
+    if not x.is_cuda:
+        raise ValueError("gdraa: tensor arguments must live on a CUDA device")
+    if not x.is_contiguous():
+        raise ValueError("gdraa: tensor arguments must be contiguous")
     return x.data_ptr()
 
 
@@ -207,15 +213,25 @@ def _ptr_array(xs):
     return (_vp * len(xs))(*[_ptr(x) for x in xs])
 
 
+def _same_numel(n, *lists):
+    """Every virtual rank's buffers hold n elements (the library trusts n)."""
+    for xs in lists:
+        for x in xs:
+            if not isinstance(x, int) and x.numel() != n:
+                raise ValueError(f"gdraa: virtual-rank buffers differ in length ({x.numel()} != {n})")
+
+
 def gdraa_vr_allreduce_mean(bufs, stream=None):
     """`len(bufs)` virtual ranks on one GPU, one cooperative launch."""
     n = bufs[0].numel()
+    _same_numel(n, bufs)
     _check(_lib.gdraa_vr_allreduce_mean(len(bufs), _ptr_array(bufs), n, dtype_code(bufs[0]),
                                         _stream(stream)), "gdraa_vr_allreduce_mean")
 
 
 def gdraa_vr_sgd_step(w, g, v, lr: float, mom: float, stream=None):
     n = g[0].numel()
+    _same_numel(n, w, g, v)
     _check(_lib.gdraa_vr_sgd_step(len(g), _ptr_array(w), _ptr_array(g), _ptr_array(v), n,
                                   dtype_code(g[0]), lr, mom, _stream(stream)),
            "gdraa_vr_sgd_step")
@@ -223,6 +239,7 @@ def gdraa_vr_sgd_step(w, g, v, lr: float, mom: float, stream=None):
 
 def gdraa_vr_sgd_step_ex(w, g, v, lr: float, mom: float, wd: float, stream=None):
     n = g[0].numel()
+    _same_numel(n, w, g, v)
     _check(_lib.gdraa_vr_sgd_step_ex(len(g), _ptr_array(w), _ptr_array(g), _ptr_array(v), n,
                                      dtype_code(g[0]), lr, mom, wd, _stream(stream)),
            "gdraa_vr_sgd_step_ex")
@@ -231,6 +248,7 @@ def gdraa_vr_sgd_step_ex(w, g, v, lr: float, mom: float, wd: float, stream=None)
 def gdraa_vr_sgd_step_mp(w_master, w_model, g, v, lr: float, mom: float, wd: float = 0.0,
                          stream=None):
     n = g[0].numel()
+    _same_numel(n, w_master, w_model, g, v)
     _check(_lib.gdraa_vr_sgd_step_mp(len(g), _ptr_array(w_master), _ptr_array(w_model),
                                      _ptr_array(g), _ptr_array(v), n, dtype_code(g[0]), lr, mom,
                                      wd, _stream(stream)), "gdraa_vr_sgd_step_mp")

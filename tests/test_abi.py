@@ -87,6 +87,17 @@ def test_calls_before_init_fail_cleanly():
     assert "gdraa_init" in gdraa.gdraa_last_error()
 
 
+def test_binding_refuses_host_and_strided_tensors():
+    import torch
+    with pytest.raises(ValueError, match="CUDA"):
+        gdraa.gdraa_sgd_step(torch.zeros(8), torch.zeros(8), torch.zeros(8), 0.1, 0.9, 0)
+    with pytest.raises(ValueError):
+        gdraa.gdraa_allreduce_mean(torch.zeros(16)[::2], 0)
+    with pytest.raises(ValueError, match="differ in length"):
+        gdraa.gdraa_vr_sgd_step([torch.zeros(8)] * 2, [torch.zeros(8), torch.zeros(4)],
+                                [torch.zeros(8)] * 2, 0.1, 0.9, 0)
+
+
 def test_poly_lr_matches_oracle(golden):
     ex = golden["poly_lr"][0]
     assert gdraa.gdraa_poly_lr(ex["lr0"], ex["iter"], ex["max_iter"], ex["power"]) == \
