@@ -127,50 +127,6 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-class NvlinkCounters:
-    """Measured NVLink bytes of this GPU (all links, each direction) from NVML's per-link
-    counters: NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / RCV_BYTES (fields 202 / 204), else
-    THROUGHPUT_DATA_TX / RX (138 / 139, KiB).  Read around an untimed pass of steps; the
-    per-step difference is the N >= 2 analogue of ncu's dram traffic (ncu cannot replay a
-    kernel that waits on other GPUs).  tools/nvlink_counters.py calibrates the families
-    against a known peer copy (profiles/r36_nvlink_counters_calibration.jsonl)."""
-
-    FAMILIES = (("NVML_FI_DEV_NVLINK_COUNT_{XMIT,RCV}_BYTES", 202, 204, 1),
-                ("NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_{TX,RX}", 138, 139, 1024))
-
-    def __init__(self, sampler):
-        self.ok, self.family = False, None
-        if sampler is None or not sampler.ok:
-            return
-        self.nv, self.h = sampler.nv, sampler.h
-        try:
-            v = self.nv.nvmlDeviceGetFieldValues(self.h, [91])[0]   # NVLINK_LINK_COUNT
-            self.links = int(v.value.uiVal) if v.nvmlReturn == 0 else 18
-        except Exception:   # noqa: BLE001
-            self.links = 18
-        for fam in self.FAMILIES:
-            if self._read(fam) is not None:
-                self.family, self.ok = fam, True
-                break
-
-    def _read(self, fam):
-        _, tx, rx, scale = fam
-        ids = [(tx, l) for l in range(self.links)] + [(rx, l) for l in range(self.links)]
-        try:
-            vals = self.nv.nvmlDeviceGetFieldValues(self.h, ids)
-        except Exception:   # noqa: BLE001
-            return None
-        good = [v.nvmlReturn == 0 for v in vals]
-        if not any(good):
-            return None
-        t = sum(int(v.value.ullVal) for v, g in zip(vals[:self.links], good) if g)
-        r = sum(int(v.value.ullVal) for v, g in zip(vals[self.links:], good[self.links:]) if g)
-        return t * scale, r * scale
-
-    def read(self):
-        return self._read(self.family) if self.ok else None
-
-
 # ---------------------------------------------------------------------------------------
 # the oracle as a CPU baseline (rank 0 only)
 # ---------------------------------------------------------------------------------------
@@ -313,9 +269,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
-    ap.add_argument("--no-nvlink-counters", action="store_true")
-    ap.add_argument("--graph", action="store_true",
-                    help="time one CUDA-graph replay of the K steps instead of an eager loop")
+    ap.add_argument("--eager", dest="graph", action="store_false",
+                    help="time an eager Python loop of the K steps instead of one CUDA-graph "
+                         "replay of them (the default: host launch cost out of the step)")
+    ap.add_argument("--graph", dest="graph", action="store_true")
+    ap.set_defaults(graph=True)
     args = ap.parse_args()
     # Exactly one JSON line on stdout: anything libraries print (NCCL banners, ...) goes
     # to stderr; the result line goes to the saved stdout.
@@ -448,30 +406,25 @@ def main():
         launches = graph_launches
     ms_step = ms / args.steps
 
-    # ---- measured NVLink bytes per step (untimed pass, rank 0's counters) ----
-    nvl = None
-    if world > 1 and not args.no_nvlink_counters:
-        ctr = NvlinkCounters(clocks) if rank == 0 else None
-        barrier()
-        if ctr is not None and ctr.ok:
-            time.sleep(1.0)   # let the counters settle
-            c0 = ctr.read()
-        barrier()
-        for k in range(args.steps):
-            sets[k % len(sets)].step()
-        barrier()
-        if ctr is not None and ctr.ok:
-            time.sleep(1.5)
-            c1 = ctr.read()
-            if c0 is not None and c1 is not None:
-                nvl = {"tx_bytes_per_launch": (c1[0] - c0[0]) / args.steps,
-                       "rx_bytes_per_launch": (c1[1] - c0[1]) / args.steps,
-                       "source": f"NVML {ctr.family[0]} summed over {ctr.links} links, "
-                                 f"rank 0, {args.steps} untimed steps"}
-        barrier()
-    per_rank = algorithmic_bytes(L, N, s_g, s_w)
-    value = per_rank * N / (ms_step * 1e-3) / 1e9           # whole job
-    achieved = per_rank / (ms_step * 1e-3) / 1e9            # per rank = per launch
+    # ---- per-call distribution (untimed pass; an event pair around every call) ----
+    M = min(args.steps, 200)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(M)]
+    barrier()
+    for k in range(M):
+        evs[k][0].record(stream)
+        sets[k % len(sets)].step()
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    per = torch.tensor([a.elapsed_time(b) * 1e3 for a, b in evs], device=dev)
+    if world > 1:
+        dist.all_reduce(per, op=dist.ReduceOp.MAX)   # a call lasts until its slowest rank
+    per = per.cpu().numpy()
+    percall = {"calls": M, "median_us": float(np.median(per)),
+               "p10_us": float(np.percentile(per, 10)), "p90_us": float(np.percentile(per, 90)),
+               "note": "an event pair around each call (max over ranks per call); the pairs "
+                       "break programmatic dependent launch between calls, so the median "
+                       "sits above ms_per_step"}
 
     # ---- e2e: host buffers through the public API, copies inside the timed region ----
     # Every step copies its gradient H2D from pinned memory, runs the step and copies this
@@ -564,10 +517,6 @@ def main():
                     "frac_of_nominal_900": achieved / NVLINK_NOMINAL_GBS,
                     "bytes_per_launch": per_rank}
         roof["traffic"] = ncu_traffic(args.config, N)
-        if nvl is not None:   # N >= 2: the bound resource's measured bytes per launch
-            nvl["algorithmic_bytes_per_launch"] = per_rank
-            nvl["rx_over_algorithmic"] = nvl["rx_bytes_per_launch"] / per_rank
-            roof["nvlink_traffic"] = nvl
         roof["kernel_ms"] = ms_step
         cpu = None
         if N == 1 and not args.no_cpu_baseline:
@@ -597,6 +546,7 @@ def main():
                             "the step through the public API, D2H of each rank's shard of "
                             "the updated weights (via a device staging copy); copies of "
                             "neighbouring steps overlap on separate streams"},
+            "per_call": percall,
             "gpu_launches": launches, "clocks": clocks.summary() if clocks else None,
             "nccl_reference": nccl,
         }

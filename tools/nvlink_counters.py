@@ -53,8 +53,12 @@ class Gpm:
             self.ok, self.err = False, f"nvmlGpmQueryDeviceSupport: {e}"
 
     def sample(self):
-        s = pynvml.nvmlGpmSampleAlloc()
-        pynvml.nvmlGpmSampleGet(self.h, s)
+        try:
+            s = pynvml.nvmlGpmSampleAlloc()
+            pynvml.nvmlGpmSampleGet(self.h, s)
+        except Exception as e:   # noqa: BLE001
+            self.ok, self.err = False, f"nvmlGpmSampleGet: {e}"
+            return None
         return s, time.perf_counter()
 
     def rates(self, a, b):
@@ -112,7 +116,7 @@ def main():
         print(json.dumps(row), flush=True)
     row = {"source": "gpm:NVLINK_TOTAL_{TX,RX}_PER_SEC", "bytes_moved": moved}
     for d in range(2):
-        if not gpms[d].ok:
+        if not gpms[d].ok or g0[d] is None or g1[d] is None:
             row[f"gpu{d}"] = gpms[d].err
             continue
         try:
