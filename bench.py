@@ -250,7 +250,8 @@ def config_dict(args, L, g_dt, desc, N, path=None):
                    f"inputs larger than L2: {args.sets} rotating (g, w, v) sets per rank "
                    f"({args.sets * L * (s_g + 8 + (2 if mp else 0)) / 1e6:.0f} MB)"),
             "path": path,
-            "timing": ("one CUDA-graph replay of the K steps" if getattr(args, "graph", False)
+            "timing": ("host wall clock of the CPU oracle per step" if args.impl == "reference"
+                       else "one CUDA-graph replay of the K steps" if args.graph
                        else "eager Python loop of the K steps")}
 
 
@@ -405,6 +406,9 @@ def main():
     if graph is not None:   # replays do not pass through the host launch counter
         launches = graph_launches
     ms_step = ms / args.steps
+    per_rank = algorithmic_bytes(L, N, s_g, s_w)
+    value = per_rank * N / (ms_step * 1e-3) / 1e9           # whole job
+    achieved = per_rank / (ms_step * 1e-3) / 1e9            # per rank = per launch
 
     # ---- per-call distribution (untimed pass; an event pair around every call) ----
     M = min(args.steps, 200)

@@ -90,7 +90,10 @@ def main():
                 "timing": "cuda_graph_replay" if args.graph else "eager_python_loop",
                 "gdraa_us": t_ours * 1e3, "gdraa_busbw_gbs": bus(t_ours),
                 "nccl_us": t_nccl * 1e3, "nccl_busbw_gbs": bus(t_nccl),
-                "speedup_vs_nccl": t_nccl / t_ours, "max_rel_diff_vs_nccl": rel}
+                "speedup_vs_nccl": t_nccl / t_ours, "max_rel_diff_vs_nccl": rel,
+                "nccl_env": {k: os.environ[k] for k in ("NCCL_ALGO", "NCCL_PROTO",
+                                                         "NCCL_NVLS_ENABLE")
+                             if k in os.environ}}
         assert rel <= 1e-5, line
         if rank == 0:
             print(json.dumps(line), file=out, flush=True)
