@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--max-log2", type=int, default=30)
     ap.add_argument("--out", default=None)
     ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays")
+    ap.add_argument("--nccl-op", choices=["avg", "sum"], default="avg",
+                    help="NCCL op timed (the result check always uses AVG)")
     args = ap.parse_args()
     out = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
@@ -83,7 +85,9 @@ def main():
         rel = float(((ours - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item())
         iters = 1000 if nbytes <= (1 << 20) else (200 if nbytes <= (1 << 26) else 20)
         t_ours = timed(lambda: gdraa.gdraa_allreduce_mean(ours), iters)   # current stream
-        t_nccl = timed(lambda: dist.all_reduce(ref, op=dist.ReduceOp.AVG), iters)
+        # timed op: AVG (same semantics) or SUM (lets NCCL pick NVLS in-switch reduction)
+        nop = dist.ReduceOp.SUM if args.nccl_op == "sum" else dist.ReduceOp.AVG
+        t_nccl = timed(lambda: dist.all_reduce(ref, op=nop), iters)
         gdraa.gdraa_deregister(ours)
         bus = lambda ms: 2 * (world - 1) / world * nbytes / (ms * 1e-3) / 1e9  # noqa: E731
         line = {"n_gpus": world, "bytes": nbytes, "iters": iters,
@@ -91,6 +95,7 @@ def main():
                 "gdraa_us": t_ours * 1e3, "gdraa_busbw_gbs": bus(t_ours),
                 "nccl_us": t_nccl * 1e3, "nccl_busbw_gbs": bus(t_nccl),
                 "speedup_vs_nccl": t_nccl / t_ours, "max_rel_diff_vs_nccl": rel,
+                "nccl_op": args.nccl_op,
                 "nccl_env": {k: os.environ[k] for k in ("NCCL_ALGO", "NCCL_PROTO",
                                                          "NCCL_NVLS_ENABLE")
                              if k in os.environ}}
