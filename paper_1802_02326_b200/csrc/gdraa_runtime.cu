@@ -565,9 +565,35 @@ int gdraa_shard(int world, int rank, size_t n, size_t *off, size_t *len) {
     return GDRAA_OK;
 }
 
+// Frees everything gdraa_init acquired (socket, peer mappings, pads, pages) and resets
+// the state; used by gdraa_finalize and when gdraa_init fails part-way.
+static void release_resources() {
+    if (g.sock >= 0) ::close(g.sock);
+    for (auto &kv : g.opened) cudaIpcCloseMemHandle(kv.second);
+    if (g.pad) cudaFree(g.pad);
+    if (g.ll) cudaFree(g.ll);
+    if (g.page_registered) cudaHostUnregister(g.page);
+    if (g.page) munmap(g.page, 4096);
+    if (g.err_h) cudaFreeHost(g.err_h);
+    State s;
+    g = s;
+}
+
+static int init_impl(int world, int rank);
+
 int gdraa_init(int world, int rank) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (g.inited) return fail(GDRAA_ESTATE, "already initialised (world %d, rank %d)", g.world, g.rank);
+    const int rc = init_impl(world, rank);
+    if (rc != GDRAA_OK) {   // leave nothing half-built behind (a retry starts clean)
+        const std::string keep = t_err;
+        release_resources();
+        t_err = keep;
+    }
+    return rc;
+}
+
+static int init_impl(int world, int rank) {
     if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
         return fail(GDRAA_EINVAL, "world %d / rank %d out of range [1,%d]", world, rank, kMaxWorld);
     State s;
@@ -906,18 +932,8 @@ int gdraa_finalize(void) {
                 keep = t_err;
             }
         }
-        ::close(g.sock);
-        g.sock = -1;
     }
-    for (auto &kv : g.opened) cudaIpcCloseMemHandle(kv.second);
-    g.opened.clear();
-    if (g.pad) cudaFree(g.pad);
-    if (g.ll) cudaFree(g.ll);
-    if (g.page_registered) cudaHostUnregister(g.page);
-    if (g.page) munmap(g.page, 4096);
-    if (g.err_h) cudaFreeHost(g.err_h);
-    State s;
-    g = s;
+    release_resources();
     t_err = keep;
     return rc;
 }

@@ -87,6 +87,21 @@ def test_calls_before_init_fail_cleanly():
     assert "gdraa_init" in gdraa.gdraa_last_error()
 
 
+def test_failed_init_leaves_clean_state():
+    """Without a usable GPU gdraa_init fails with ECUDA; it must not leave a half-built
+    state behind: a retry fails the same way (not ESTATE) and no call sees a communicator."""
+    from tests.conftest import has_cuda
+    if has_cuda():
+        pytest.skip("needs a machine without a GPU")
+    for _ in range(2):
+        with pytest.raises(gdraa.GdraaError) as e:
+            gdraa.gdraa_init(1, 0)
+        assert e.value.name == "GDRAA_ECUDA"
+    with pytest.raises(gdraa.GdraaError) as e:
+        gdraa.gdraa_get_stats()
+    assert e.value.name == "GDRAA_ESTATE"
+
+
 def test_binding_refuses_host_and_strided_tensors():
     import torch
     with pytest.raises(ValueError, match="CUDA"):
