@@ -74,7 +74,8 @@ typedef enum {
  * communicator's lifetime and checked to agree on every rank, since they decide which
  * kernel -- with which synchronisation protocol -- serves a call.
  * Errors: EINVAL (range), ESTATE (already initialised), ESHAPE (ranks disagree on the
- * thresholds), EJOBSERVER, ECUDA.
+ * thresholds), EJOBSERVER, ECUDA.  A failed call releases whatever it had acquired
+ * (pads, mappings, socket), so it may be retried.
  */
 int gdraa_init(int world, int rank);
 
