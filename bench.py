@@ -520,6 +520,13 @@ def main():
                     "peak_source": "measured B200 peer copy per direction (B200_PROFILING.md)",
                     "frac_of_nominal_900": achieved / NVLINK_NOMINAL_GBS,
                     "bytes_per_launch": per_rank}
+            # the HBM side of the same launch: all of g read once (locally
+            # or by peers), the owner shard's w / master and v read+written, and every
+            # w' (or bf16 copy) element written once into this rank's memory
+            hb = (s_g * L + (16 if mp else 12) * L / N + s_w * L)
+            roof["hbm_side"] = {"bytes_per_launch": hb,
+                                "achieved_gbs": hb / (ms_step * 1e-3) / 1e9,
+                                "frac_of_peak": hb / (ms_step * 1e-3) / 1e9 / peaks["hbm_gbs"]}
         roof["traffic"] = ncu_traffic(args.config, N)
         roof["kernel_ms"] = ms_step
         cpu = None
