@@ -487,6 +487,29 @@ def main():
         ems = float(t.item())
     e2e_val = per_rank * N / (ems / args.e2e_steps * 1e-3) / 1e9
 
+    # the same per-step copies alone (H2D and D2H concurrently, no step): the PCIe bound
+    # the e2e figure is held to
+    barrier()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    s_h2d.wait_event(c0)
+    s_d2h.wait_event(c0)
+    for k in range(args.e2e_steps):
+        with torch.cuda.stream(s_h2d):
+            g_bufs[k % 2].copy_(g_host[k % 2], non_blocking=True)
+        with torch.cuda.stream(s_d2h):
+            out_host[k % 2].copy_(stage[k % 2], non_blocking=True)
+    stream.wait_stream(s_h2d)
+    stream.wait_stream(s_d2h)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    cms = c0.elapsed_time(c1)
+    if world > 1:
+        t = torch.tensor([cms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        cms = float(t.item())
+    copy_bound = per_rank * N / (cms / args.e2e_steps * 1e-3) / 1e9
+
     # ---- NCCL all_reduce(AVG) of the same gradient buffer (reference point) ----
     nccl = None
     if world > 1 and not args.no_nccl:
@@ -556,7 +579,11 @@ def main():
                     "note": "all ranks: H2D of each rank's gradient from pinned host memory, "
                             "the step through the public API, D2H of each rank's shard of "
                             "the updated weights (via a device staging copy); copies of "
-                            "neighbouring steps overlap on separate streams"},
+                            "neighbouring steps overlap on separate streams",
+                    "copies_only_value": copy_bound,
+                    "frac_of_copies_only": e2e_val / copy_bound,
+                    "copies_only_note": "the same H2D + D2H copies alone, no step: the PCIe "
+                                        "bound of this e2e figure, in the same units"},
             "per_call": percall,
             "gpu_launches": launches, "clocks": clocks.summary() if clocks else None,
             "nccl_reference": nccl,
