@@ -857,15 +857,11 @@ struct TmaCfg {
     static constexpr int THREADS = 32 * (CW + 1);
     static constexpr int STAGE_BYTES = CH * PER_EL;
     static constexpr int SMEM = STAGES * STAGE_BYTES;
-    // a 3-stage ring leaves room for a second CTA per SM (the next call's, under PDL) if
-    // the registers fit too: ask ptxas for that
-    static constexpr int MINB = ST_ == 3 ? 2 : 1;
 };
 
 template <typename TG, int WORLD, int MODE, int CW_ = 16, int ST_ = 4, int TAILDIV_ = 4,
           int TDEPTH_ = ST_, int ROT_ = 0>
-__global__ void __launch_bounds__(TmaCfg<TG, WORLD, MODE, CW_, ST_, TAILDIV_, TDEPTH_, ROT_>::THREADS,
-                                  (TmaCfg<TG, WORLD, MODE, CW_, ST_, TAILDIV_, TDEPTH_, ROT_>::MINB))
+__global__ void __launch_bounds__(TmaCfg<TG, WORLD, MODE, CW_, ST_, TAILDIV_, TDEPTH_, ROT_>::THREADS, 1)
 gdraa_tma_kernel(const __grid_constant__ KParams p) {
     using C = TmaCfg<TG, WORLD, MODE, CW_, ST_, TAILDIV_, TDEPTH_, ROT_>;
     using EL = Elem<TG>;
@@ -1145,33 +1141,8 @@ struct TmaLaunch {
     int ch;
 };
 
-// GDRAA_TMA_STAGES=3 (A/B only, N = 2..4): a 3-stage ring instead of 4, so that with
-// GDRAA_TMA_PER_SM=1 a CTA of the next back-to-back call fits beside the running one and
-// waits at griddepcontrol.wait instead of being launched after it exits.
-int env_tma_stages() {
-    static const int v = [] {
-        const char *e = std::getenv("GDRAA_TMA_STAGES");
-        return e != nullptr && e[0] == '3' ? 3 : 4;
-    }();
-    return v;
-}
-
-int env_tma_per_sm() {
-    static const int v = [] {
-        const char *e = std::getenv("GDRAA_TMA_PER_SM");
-        return e != nullptr ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
 template <typename TG, int MODE, int WORLD>
 TmaLaunch pick_tma_w() {
-    if constexpr (WORLD >= 2 && WORLD <= 4) {
-        if (env_tma_stages() == 3) {
-            using C3 = TmaCfg<TG, WORLD, MODE, 16, 3>;
-            return {gdraa_tma_kernel<TG, WORLD, MODE, 16, 3>, C3::THREADS, C3::SMEM, C3::CH};
-        }
-    }
     using C = TmaCfg<TG, WORLD, MODE>;
     return {gdraa_tma_kernel<TG, WORLD, MODE>, C::THREADS, C::SMEM, C::CH};
 }
@@ -1456,7 +1427,6 @@ cudaError_t launch_gdraa_tma(const KParams &p, int dtype, int mode, int vr_rows,
     }
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    if (env_tma_per_sm() > 0 && env_tma_per_sm() < per_sm) per_sm = env_tma_per_sm();
     int cap = sms * per_sm / vr_rows;
     const int env_cap = env_max_ctas();
     if (env_cap > 0 && env_cap < cap) cap = env_cap;
