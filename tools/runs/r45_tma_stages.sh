@@ -1,3 +1,5 @@
+# OUTCOME (r45): all variants within +-0.8%; the GDRAA_TMA_STAGES / GDRAA_TMA_PER_SM knobs
+# existed only for this A/B (commit 51c0220) and were removed afterwards.
 # A/B: TMA ring depth 4 (default, 128 KB smem: one CTA per SM) vs 3 stages (96 KB), the
 # latter with the grid at 2 CTAs/SM or capped at 1/SM so the next call's CTAs (PDL) fit
 # beside the running ones; N=2 and N=4, R50 and R101 fp32, graph-timed bench
