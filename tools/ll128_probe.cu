@@ -15,7 +15,7 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/ll128_probe \
 //        tools/ll128_probe.cu
-//   tools/ll128_probe [lines_per_epoch=262144] [epochs=200]
+//   tools/ll128_probe [lines_per_epoch=262144] [epochs=200] [control=0]
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -62,8 +62,11 @@ __device__ __forceinline__ void st_rel(uint64_t *p, uint64_t v) {
 
 // Persistent sender: every thread owns 16 bytes of a line per step; a grid-wide epoch
 // loop waits for the receiver's ack of e - 1 (one poller per CTA) before writing epoch e.
+// control = 1 (negative control, validates the detector): the flag lane stores its flag
+// word first, in its own instruction, and the line's payload afterwards -- a reader can
+// then see the new flag with old payload, and torn_lines must come out > 0.
 __global__ void sender(uint64_t *remote, uint64_t lines, int epochs, const uint64_t *ack,
-                       unsigned *gave_up) {
+                       unsigned *gave_up, int control) {
     const uint64_t tid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t nthr = gridDim.x * blockDim.x;
     const int j = threadIdx.x & 7;   // lane within the 8-lane line group
@@ -82,7 +85,23 @@ __global__ void sender(uint64_t *remote, uint64_t lines, int epochs, const uint6
             const uint64_t line = t >> 3;
             const uint64_t a = tag(e, line, 2 * j);
             const uint64_t b = j == 7 ? e : tag(e, line, 2 * j + 1);
-            st_v2(remote + line * 16 + 2 * j, a, b);
+            if (control) {
+                if (j == 7) {
+                    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(remote + line * 16 + 15),
+                                 "l"(e)
+                                 : "memory");
+                    __nanosleep(200);
+                }
+                __syncwarp();
+                if (j == 7)
+                    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(remote + line * 16 + 14),
+                                 "l"(a)
+                                 : "memory");
+                else
+                    st_v2(remote + line * 16 + 2 * j, a, b);
+            } else {
+                st_v2(remote + line * 16 + 2 * j, a, b);
+            }
         }
     }
 }
@@ -143,6 +162,7 @@ __global__ void receiver(const uint64_t *buf, uint64_t lines, int epochs, uint64
 int main(int argc, char **argv) {
     const uint64_t lines = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 262144;
     const int epochs = argc > 2 ? std::atoi(argv[2]) : 200;
+    const int control = argc > 3 ? std::atoi(argv[3]) : 0;
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
     if (ndev < 2) {
@@ -181,7 +201,7 @@ int main(int argc, char **argv) {
     CK(cudaGetLastError());
     CK(cudaSetDevice(0));
     CK(cudaEventRecord(t0));
-    sender<<<sms, 256>>>(buf, lines, epochs, ack, gave_up_s);
+    sender<<<sms, 256>>>(buf, lines, epochs, ack, gave_up_s, control);
     CK(cudaGetLastError());
     CK(cudaEventRecord(t1));
     CK(cudaDeviceSynchronize());
@@ -196,10 +216,10 @@ int main(int argc, char **argv) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, t0, t1));
     const double bytes = static_cast<double>(lines) * 128 * epochs;
-    std::printf("{\"probe\": \"ll128_line_atomicity\", \"lines_per_epoch\": %llu, \"epochs\": %d, "
+    std::printf("{\"probe\": \"ll128_line_atomicity\", \"control\": %d, \"lines_per_epoch\": %llu, \"epochs\": %d, "
                 "\"lines_checked\": %.0f, \"torn_lines\": %llu, \"polls\": %llu, "
                 "\"sender_ms\": %.3f, \"gbs_one_way_incl_acks\": %.1f, \"gave_up\": [%u, %u]}\n",
-                static_cast<unsigned long long>(lines), epochs,
+                control, static_cast<unsigned long long>(lines), epochs,
                 static_cast<double>(lines) * epochs, h[0], h[1], ms, bytes / (ms * 1e-3) / 1e9, gu[0],
                 gu[1]);
     return 0;
