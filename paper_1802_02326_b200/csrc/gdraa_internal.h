@@ -94,6 +94,8 @@ bool use_tma_kernel(int dtype, int mode, int world);
 // Requires n * elem_size <= 8 * p.ll_pairs.
 cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool cooperative,
                             cudaStream_t s);
+// GDRAA_LL128=1: launch_gdraa_ll uses the LL128 line format (read once per process).
+bool use_ll128();
 
 // Small-message fused SGD step (kSgd / kSgdMp): gradient blocks and updated blocks travel
 // as LL entries through the same receive areas; the data carries both synchronisations.

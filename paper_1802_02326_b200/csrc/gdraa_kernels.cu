@@ -614,6 +614,111 @@ gdraa_ll_kernel(const __grid_constant__ KParams p) {
 }
 
 // ---------------------------------------------------------------------------------
+// LL128 variant of the small-message allreduce_mean (opt-in: GDRAA_LL128=1, must match on
+// every rank; checked at gdraa_init).  Same receive slots, same parity rule, same fold;
+// the slot is used as 128-byte lines of 120 payload bytes + an 8-byte flag {flag, flag}
+// instead of 16-byte entries of 8 payload bytes + two flags.  Lane j (0..7) of an 8-lane
+// group owns bytes [16j, 16j+16) of one line and stores / loads them with one 16-byte
+// access, so each line moves in one warp instruction; lane 7 carries the flag.  A flag
+// seen implies the whole line is there only because NVLink delivers such a line whole --
+// measured, not architected: profiles/r46_ll128_probe.jsonl (0 torn lines in 567 M racing
+// reads; the negative control tears 70-88%).  Line k holds payload pairs [15k, 15k+15).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ const uint4 *ll128_slot(const uint4 *slot) {
+    return reinterpret_cast<const uint4 *>((reinterpret_cast<uintptr_t>(slot) + 127) & ~uintptr_t(127));
+}
+
+template <typename TG, int WORLD>
+__global__ void __launch_bounds__(512, 2)   // 2 CTAs/SM: launch_gdraa_ll's resident grid
+gdraa_ll128_kernel(const __grid_constant__ KParams p) {
+    const int vr = blockIdx.y;
+    const int rank = p.rank0 + vr;
+    Pad *mine = p.pad[vr][rank];
+    __shared__ int s_last;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint64_t epoch = *reinterpret_cast<volatile uint64_t *>(&mine->epoch) + 1;
+    const uint32_t flag = static_cast<uint32_t>(epoch);
+    const uint64_t par = epoch & 1u;
+    const uint64_t nbytes = p.n * sizeof(TG);
+    const uint64_t nlines = (nbytes + 119) / 120;
+    void *const buf = p.dst[vr][rank];
+    const int j = threadIdx.x & 7;
+    const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+    const uint64_t groups = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 8);
+    bool ok = true;
+    // group-uniform loop: every lane of an 8-lane group handles the same line k
+    for (uint64_t k = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 8;
+         k < nlines; k += groups) {
+        const uint64_t pr = 15 * k + 2 * j;                 // first payload pair of this lane
+        const uint2 a = load_pair(buf, pr, nbytes);
+        const uint2 b = j < 7 ? load_pair(buf, pr + 1, nbytes) : make_uint2(flag, flag);
+        const uint4 entry = make_uint4(a.x, a.y, b.x, b.y);
+#pragma unroll
+        for (int kk = 1; kk < WORLD; ++kk) {   // push the line to every peer's slot [par][rank]
+            const int q = (rank + kk) % WORLD;
+            uint4 *dst = const_cast<uint4 *>(ll128_slot(p.ll[vr][q] + (par * WORLD + rank) * p.ll_pairs));
+            st_ll(dst + k * 8 + j, entry);
+        }
+        uint32_t w[4][WORLD];
+#pragma unroll
+        for (int q = 0; q < WORLD; ++q) {
+            uint4 r = entry;
+            if (q != rank) {
+                const uint4 *src = ll128_slot(p.ll[vr][rank] + (par * WORLD + q) * p.ll_pairs) + k * 8 + j;
+                const uint64_t t0 = global_timer_ns();
+                uint32_t polls = 0, sleep_ns = 32;
+                while (true) {
+                    r = ld_ll(src);
+                    const bool here = __shfl_sync(gmask, r.z == flag && r.w == flag, 7, 8);
+                    if (here) break;
+                    bool late = false;
+                    if ((++polls & 1023u) == 0)
+                        late = global_timer_ns() - t0 > p.timeout_ns ||
+                               (p.abort != nullptr && *p.abort != 0);
+                    if (__shfl_sync(gmask, late, 0, 8)) {
+                        ok = false;
+                        break;
+                    }
+                    if (p.ll_sleep_ns != 0) {
+                        __nanosleep(sleep_ns);
+                        sleep_ns = sleep_ns * 2 > p.ll_sleep_ns ? p.ll_sleep_ns : sleep_ns * 2;
+                    }
+                }
+                if (!ok) {
+                    if (j == 0) report_timeout(p.err, 1, q, vr);
+                    break;
+                }
+            }
+            w[0][q] = r.x;
+            w[1][q] = r.y;
+            w[2][q] = r.z;
+            w[3][q] = r.w;
+        }
+        if (!ok) break;
+        store_pair(buf, pr, nbytes,
+                   make_uint2(WordMean<TG, WORLD>::run(w[0]), WordMean<TG, WORLD>::run(w[1])));
+        if (j < 7)
+            store_pair(buf, pr + 1, nbytes,
+                       make_uint2(WordMean<TG, WORLD>::run(w[2]), WordMean<TG, WORLD>::run(w[3])));
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&mine->arrive, 1u);
+        s_last = (prev == gridDim.x - 1);
+        if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        mine->arrive = 0;
+        mine->calls += 1;
+        mine->ll_calls += 1;
+        mine->epoch = epoch;
+        if (p.done[vr] != nullptr) *p.done[vr] = epoch;
+    }
+}
+
+// ---------------------------------------------------------------------------------
 // Small-message fused SGD step (the latency path of gdraa_sgd_step / _mp).  The
 // momentum is owner-sharded (AMB-19), so the one-shot scheme above cannot serve it; this
 // kernel keeps the two-shot structure of Algorithm 1 but lets the data carry the
@@ -1134,6 +1239,20 @@ KernelFnLL pick_ll_t(int world) {
     }
 }
 
+template <typename TG>
+KernelFnLL pick_ll128_t(int world) {
+    switch (world) {
+        case 2: return gdraa_ll128_kernel<TG, 2>;
+        case 3: return gdraa_ll128_kernel<TG, 3>;
+        case 4: return gdraa_ll128_kernel<TG, 4>;
+        case 5: return gdraa_ll128_kernel<TG, 5>;
+        case 6: return gdraa_ll128_kernel<TG, 6>;
+        case 7: return gdraa_ll128_kernel<TG, 7>;
+        case 8: return gdraa_ll128_kernel<TG, 8>;
+        default: return nullptr;
+    }
+}
+
 struct TmaLaunch {
     KernelFnLL fn;
     int threads;
@@ -1300,15 +1419,29 @@ cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows, boo
     return launch_pdl(l.fn, grid, block, s, p);
 }
 
+bool use_ll128() {
+    static const bool v = [] {
+        const char *e = std::getenv("GDRAA_LL128");
+        return e != nullptr && e[0] == '1';
+    }();
+    return v;
+}
+
 cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool cooperative,
                             cudaStream_t s) {
-    KernelFnLL fn = dtype == GDRAA_F32 ? pick_ll_t<float>(p.world)
-                                       : pick_ll_t<__nv_bfloat16>(p.world);
+    const bool l128 = use_ll128();
+    KernelFnLL fn = l128 ? (dtype == GDRAA_F32 ? pick_ll128_t<float>(p.world)
+                                               : pick_ll128_t<__nv_bfloat16>(p.world))
+                         : (dtype == GDRAA_F32 ? pick_ll_t<float>(p.world)
+                                               : pick_ll_t<__nv_bfloat16>(p.world));
     if (fn == nullptr) return cudaErrorInvalidValue;
     const uint64_t es = dtype == GDRAA_F32 ? 4 : 2;
     if (p.n * es > 8 * p.ll_pairs) return cudaErrorInvalidValue;
+    // LL128: lines from the first 128-byte boundary of the slot must fit in it
+    if (l128 && 128 + (p.n * es + 119) / 120 * 128 > 16 * p.ll_pairs) return cudaErrorInvalidValue;
     constexpr int kT = 512;
-    const uint64_t npairs = (p.n * es + 7) / 8;
+    // threads needed: one per 8-byte pair (LL) or 8 per 120-byte line (LL128)
+    const uint64_t npairs = l128 ? (p.n * es + 119) / 120 * 8 : (p.n * es + 7) / 8;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -700,13 +700,14 @@ static int init_impl(int world, int rank) {
     if (world > 1) {
         proto::Reg cfg{};
         cfg.what = 3;
-        cfg.n = g.ll_sgd_limit;
+        cfg.n = g.ll_sgd_limit | (use_ll128() ? 1ull << 63 : 0ull);   // + the LL format
         cfg.dtype = static_cast<int32_t>(std::min<uint64_t>(g.ll_pairs, INT32_MAX));
         proto::RegOk all{};
         int rc = exchange(cfg, &all);
         if (rc == GDRAA_ESHAPE)
             rc = fail(GDRAA_ESHAPE, "ranks disagree on the small-message thresholds "
-                      "(GDRAA_LL_MAX_BYTES / GDRAA_LL_SGD_MAX_BYTES must match on every rank): %s",
+                      "(GDRAA_LL_MAX_BYTES / GDRAA_LL_SGD_MAX_BYTES / GDRAA_LL128 must match on every "
+                      "rank): %s",
                       t_err.c_str());
         if (rc) return cleanup_fail(rc);
     }

@@ -1,0 +1,45 @@
+"""Run by test_gpu_kernels.py in a subprocess with GDRAA_LL128=1 (read once per process):
+virtual-rank parity of the LL128 line format of the small-message allreduce_mean -- every
+world size, both dtypes, ragged sizes around the 120-byte line and up to the LL
+threshold, and chains of calls (the two slot parities alternate)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+from paper_1802_02326_b200 import gdraa  # noqa: E402
+from tests._parity import compare  # noqa: E402
+from tests.test_gpu_parity import from_dev, make_grads, to_dev  # noqa: E402
+
+
+def main():
+    assert os.environ.get("GDRAA_LL128") == "1"
+    count = 0
+    for N in range(2, 9):
+        lim = gdraa.gdraa_small_message_bytes(N)
+        for dt in ("f32", "bf16"):
+            bf16 = dt == "bf16"
+            es = 2 if bf16 else 4
+            sizes = [1, 2, 3, 29, 30, 31, 59, 60, 61, 257, 4097, 70_001, lim // es]
+            if bf16:
+                sizes += [119, 120, 121]
+            for i, L in enumerate(sizes):
+                for fam in ("like", "int"):
+                    for step in range(3 if L == 4097 else 1):   # chained: both parities
+                        gs = make_grads(fam, 900 + 10 * N + i + 100 * step, N, L, bf16)
+                        bufs = [to_dev(g, bf16) for g in gs]
+                        gdraa.gdraa_vr_allreduce_mean(bufs)
+                        torch.cuda.synchronize()
+                        exp = oracle.allreduce_mean(gs)
+                        for r in range(N):
+                            compare(from_dev(bufs[r]), exp, dt,
+                                    what=f"ll128 mean N={N} {dt} L={L} {fam} r{r}")
+                        count += 1
+    print(f"OK ll128 {count} cases")
+
+
+if __name__ == "__main__":
+    main()

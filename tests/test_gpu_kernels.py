@@ -22,3 +22,12 @@ def test_forced_kernel_parity(kernel):
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert f"OK {kernel}" in r.stdout
+
+
+def test_ll128_mean_parity():
+    """The opt-in LL128 line format of the small-message mean gives the oracle's bits."""
+    env = dict(os.environ, GDRAA_LL128="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_ll128_worker.py")],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "OK ll128" in r.stdout
