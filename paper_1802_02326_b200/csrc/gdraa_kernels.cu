@@ -623,6 +623,8 @@ gdraa_ll_kernel(const __grid_constant__ KParams p) {
 // seen implies the whole line is there only because NVLink delivers such a line whole --
 // measured, not architected: profiles/r46_ll128_probe.jsonl (0 torn lines in 567 M racing
 // reads; the negative control tears 70-88%).  Line k holds payload pairs [15k, 15k+15).
+// The receiver zeroes every line it consumed: the small-message SGD kernel uses the same
+// slots in the LL format, whose flag test a stale LL128 payload word must never satisfy.
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ const uint4 *ll128_slot(const uint4 *slot) {
     return reinterpret_cast<const uint4 *>((reinterpret_cast<uintptr_t>(slot) + 127) & ~uintptr_t(127));
@@ -688,6 +690,10 @@ gdraa_ll128_kernel(const __grid_constant__ KParams p) {
                     if (j == 0) report_timeout(p.err, 1, q, vr);
                     break;
                 }
+                // consumed: clear the line, so that no stale payload word of it can ever
+                // pass for a flag of the LL-format kernels sharing this slot (the next
+                // writer of this parity comes after this call completes, as for LL)
+                st_ll(const_cast<uint4 *>(src), make_uint4(0u, 0u, 0u, 0u));
             }
             w[0][q] = r.x;
             w[1][q] = r.y;

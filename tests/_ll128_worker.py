@@ -38,6 +38,36 @@ def main():
                             compare(from_dev(bufs[r]), exp, dt,
                                     what=f"ll128 mean N={N} {dt} L={L} {fam} r{r}")
                         count += 1
+    # LL128 mean calls interleaved with small-message SGD steps (LL format) on the same
+    # receive slots: each result must still be the oracle's
+    import synth
+    for N in (2, 3, 4, 8):
+        L = 4097
+        w0, v0 = synth.w_like(950 + N, L), synth.w_like(951 + N, L)
+        w_d = [to_dev(w0) for _ in range(N)]
+        v_d = [to_dev(v0) for _ in range(N)]
+        w_ref, v_ref = w0.copy(), v0.copy()
+        for step in range(6):
+            gs = make_grads("like", 960 + 10 * N + step, N, L, False)
+            if step % 2 == 0:
+                bufs = [to_dev(g) for g in gs]
+                gdraa.gdraa_vr_allreduce_mean(bufs)
+                torch.cuda.synchronize()
+                exp = oracle.allreduce_mean(gs)
+                for r in range(N):
+                    compare(from_dev(bufs[r]), exp, "f32", what=f"mixed mean N={N} s{step} r{r}")
+            else:
+                g_d = [to_dev(g) for g in gs]
+                gdraa.gdraa_vr_sgd_step(w_d, g_d, v_d, 0.1, 0.9)
+                torch.cuda.synchronize()
+                w_ref, v_new = oracle.sgd_step(gs, w_ref, v_ref, 0.1, 0.9)
+                for r in range(N):
+                    off, ln = gdraa.gdraa_shard(N, r, L)
+                    compare(from_dev(w_d[r]), w_ref, "f32", what=f"mixed sgd w N={N} s{step}")
+                    compare(from_dev(v_d[r])[off:off + ln], v_new[off:off + ln], "f32",
+                            what=f"mixed sgd v N={N} s{step}")
+                v_ref = v_new
+            count += 1
     print(f"OK ll128 {count} cases")
 
 
