@@ -94,8 +94,12 @@ bool use_tma_kernel(int dtype, int mode, int world);
 // Requires n * elem_size <= 8 * p.ll_pairs.
 cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool cooperative,
                             cudaStream_t s);
-// GDRAA_LL128=1: launch_gdraa_ll uses the LL128 line format (read once per process).
-bool use_ll128();
+// Whether launch_gdraa_ll uses the LL128 line format for a call of nbytes per rank:
+// from kLL128MinBytes / (N-1) up (measured crossover); GDRAA_LL128=1 / 0 forces it
+// on / off (ll128_mode: 1 / 0; 2 = by size).  Read once per process.
+int ll128_mode();
+bool ll128_for(uint64_t nbytes, int world);
+constexpr uint64_t kLL128MinBytes = 512ull << 10;
 
 // Small-message fused SGD step (kSgd / kSgdMp): gradient blocks and updated blocks travel
 // as LL entries through the same receive areas; the data carries both synchronisations.

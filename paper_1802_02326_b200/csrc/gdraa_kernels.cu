@@ -614,8 +614,8 @@ gdraa_ll_kernel(const __grid_constant__ KParams p) {
 }
 
 // ---------------------------------------------------------------------------------
-// LL128 variant of the small-message allreduce_mean (opt-in: GDRAA_LL128=1, must match on
-// every rank; checked at gdraa_init).  Same receive slots, same parity rule, same fold;
+// LL128 variant of the small-message allreduce_mean (served when n * s * (N-1) >= 512 KiB;
+// GDRAA_LL128=1 / 0 forces it on / off and must match on every rank, checked at init).  Same receive slots, same parity rule, same fold;
 // the slot is used as 128-byte lines of 120 payload bytes + an 8-byte flag {flag, flag}
 // instead of 16-byte entries of 8 payload bytes + two flags.  Lane j (0..7) of an 8-lane
 // group owns bytes [16j, 16j+16) of one line and stores / loads them with one 16-byte
@@ -1425,17 +1425,27 @@ cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows, boo
     return launch_pdl(l.fn, grid, block, s, p);
 }
 
-bool use_ll128() {
-    static const bool v = [] {
+int ll128_mode() {
+    static const int v = [] {
         const char *e = std::getenv("GDRAA_LL128");
-        return e != nullptr && e[0] == '1';
+        if (e == nullptr || *e == 0) return 2;
+        return e[0] == '1' ? 1 : e[0] == '0' ? 0 : 2;
     }();
     return v;
 }
 
+bool ll128_for(uint64_t nbytes, int world) {
+    const int m = ll128_mode();
+    if (m != 2) return m == 1;
+    // measured crossover (profiles/r48_sweep_n*_ll128_*.jsonl): the line format wins from
+    // ~512 KiB at N = 2 and ~256 KiB at N = 4, where LL's 2x bytes dominate; below, the
+    // LL entries' shorter poll path wins by <= 0.8 us
+    return nbytes * static_cast<uint64_t>(world - 1) >= kLL128MinBytes;
+}
+
 cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool cooperative,
                             cudaStream_t s) {
-    const bool l128 = use_ll128();
+    const bool l128 = ll128_for(p.n * (dtype == GDRAA_F32 ? 4 : 2), p.world);
     KernelFnLL fn = l128 ? (dtype == GDRAA_F32 ? pick_ll128_t<float>(p.world)
                                                : pick_ll128_t<__nv_bfloat16>(p.world))
                          : (dtype == GDRAA_F32 ? pick_ll_t<float>(p.world)

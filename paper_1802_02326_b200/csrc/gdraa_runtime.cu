@@ -700,7 +700,7 @@ static int init_impl(int world, int rank) {
     if (world > 1) {
         proto::Reg cfg{};
         cfg.what = 3;
-        cfg.n = g.ll_sgd_limit | (use_ll128() ? 1ull << 63 : 0ull);   // + the LL format
+        cfg.n = g.ll_sgd_limit | (static_cast<uint64_t>(ll128_mode()) << 62);   // + LL format rule
         cfg.dtype = static_cast<int32_t>(std::min<uint64_t>(g.ll_pairs, INT32_MAX));
         proto::RegOk all{};
         int rc = exchange(cfg, &all);
