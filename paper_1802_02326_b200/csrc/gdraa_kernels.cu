@@ -1475,6 +1475,177 @@ cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool coope
 }
 
 namespace {
+// Poll one LL128 line (this lane's 16 bytes of it) until lane 7 of the 8-lane group sees
+// the flag; group-uniform result.  Bounded like ll_wait; on give-up ok = false.
+__device__ __forceinline__ uint4 ll128_wait(const uint4 *src, uint32_t flag, unsigned gmask,
+                                            const KParams &p, bool &ok) {
+    const uint64_t t0 = global_timer_ns();
+    uint32_t polls = 0, sleep_ns = 32;
+    while (true) {
+        const uint4 r = ld_ll(src);
+        if (__shfl_sync(gmask, r.z == flag && r.w == flag, 7, 8)) return r;
+        bool late = false;
+        if ((++polls & 1023u) == 0)
+            late = global_timer_ns() - t0 > p.timeout_ns || (p.abort != nullptr && *p.abort != 0);
+        if (__shfl_sync(gmask, late, 0, 8)) {
+            ok = false;
+            return r;
+        }
+        if (p.ll_sleep_ns != 0) {
+            __nanosleep(sleep_ns);
+            sleep_ns = sleep_ns * 2 > p.ll_sleep_ns ? p.ll_sleep_ns : sleep_ns * 2;
+        }
+    }
+}
+}  // namespace
+
+// LL128 form of the small-message SGD step for fp32 gradients and fp32 w (kSgd): the same
+// three phases, slot parity rule, fold and update as gdraa_ll_sgd_kernel, with every
+// transfer in 128-byte lines of 120 payload bytes (30 elements) + flag, as the LL128 mean.
+// Lane j of an 8-lane group owns elements [30k + 4j, +4) of line k (lane 7: 2 elements +
+// the flag); the gradient line k and the broadcast line k of a block cover the same
+// elements (4-byte g and w').  Slot of a sender: lines [0, RL) gradient block, [RL, 2RL)
+// updated block, RL = ceil(4 blk / 120).  Consumed lines are cleared (LL kernels share
+// the slots).
+template <int WORLD>
+__global__ void __launch_bounds__(512, 2)
+gdraa_ll128_sgd_kernel(const __grid_constant__ KParams p) {
+    const int vr = blockIdx.y;
+    const int rank = p.rank0 + vr;
+    Pad *mine = p.pad[vr][rank];
+    __shared__ int s_last;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint64_t epoch = *reinterpret_cast<volatile uint64_t *>(&mine->epoch) + 1;
+    const uint32_t flag = static_cast<uint32_t>(epoch);
+    const uint64_t par = epoch & 1u;
+    const uint64_t RL = (p.blk * 4 + 119) / 120;
+    const int j = threadIdx.x & 7;
+    const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+    const uint64_t g0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 8;
+    const uint64_t groups = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 8);
+    auto shard = [&](int q, uint64_t &o, uint64_t &l) {
+        o = min(static_cast<uint64_t>(q) * p.blk, p.n);
+        l = min(p.blk, p.n - o);
+    };
+    auto rx = [&](int q) {
+        return const_cast<uint4 *>(ll128_slot(p.ll[vr][rank] + (par * WORLD + q) * p.ll_pairs));
+    };
+    auto tx = [&](int q) {
+        return const_cast<uint4 *>(ll128_slot(p.ll[vr][q] + (par * WORLD + rank) * p.ll_pairs));
+    };
+    const float *const gl = static_cast<const float *>(p.src[vr][rank]);
+    bool ok = true;
+
+    // A: push block D(rank, q) to every owner q != rank.
+    #pragma unroll 1
+    for (int k = 1; k < WORLD; ++k) {
+        const int q = (rank + k) % WORLD;
+        uint64_t oq, lq;
+        shard(q, oq, lq);
+        const uint64_t nb = lq * 4, nl = (nb + 119) / 120;
+        const float *base = gl + oq;
+        uint4 *dst = tx(q);
+        for (uint64_t ln = g0; ln < nl; ln += groups) {
+            const uint64_t pr = 15 * ln + 2 * j;
+            const uint2 a = load_pair(base, pr, nb);
+            const uint2 b = j < 7 ? load_pair(base, pr + 1, nb) : make_uint2(flag, flag);
+            st_ll(dst + ln * 8 + j, make_uint4(a.x, a.y, b.x, b.y));
+        }
+    }
+
+    // B: fold + update our block line by line, push w' lines to every peer.
+    uint64_t off, len;
+    shard(rank, off, len);
+    float *const vloc = p.v[vr];
+    float *const wloc = static_cast<float *>(p.dst[vr][rank]);
+    const float lr = p.lr, mom = p.mom, wd = p.wd;
+    const uint64_t nl_own = (len * 4 + 119) / 120;
+    for (uint64_t ln = g0; ok && ln < nl_own; ln += groups) {
+        const uint64_t i0 = 30 * ln + 4 * j;                       // shard-relative
+        const int cap_e = j < 7 ? 4 : 2;
+        const int cnt = i0 >= len ? 0 : static_cast<int>(len - i0 < static_cast<uint64_t>(cap_e)
+                                                             ? len - i0 : cap_e);
+        float x[WORLD][4];
+#pragma unroll
+        for (int q = 0; q < WORLD; ++q) {
+            if (q == rank) {
+                for (int e = 0; e < 4; ++e) x[q][e] = e < cnt ? gl[off + i0 + e] : 0.f;
+                continue;
+            }
+            uint4 *src = rx(q) + ln * 8 + j;
+            const uint4 r = ll128_wait(src, flag, gmask, p, ok);
+            if (!ok) {
+                if (j == 0) report_timeout(p.err, 1, q, vr);
+                break;
+            }
+            st_ll(src, make_uint4(0u, 0u, 0u, 0u));
+            x[q][0] = __uint_as_float(r.x);
+            x[q][1] = __uint_as_float(r.y);
+            x[q][2] = __uint_as_float(r.z);
+            x[q][3] = __uint_as_float(r.w);
+        }
+        if (!ok) break;
+        uint32_t ow[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (e >= cnt) break;
+            float col[WORLD];
+#pragma unroll
+            for (int q = 0; q < WORLD; ++q) col[q] = x[q][e];
+            const float m = average<WORLD>(col);
+            float wv = wloc[off + i0 + e], vv = vloc[off + i0 + e];
+            sgd(m, lr, mom, wd, wv, vv);
+            vloc[off + i0 + e] = vv;
+            wloc[off + i0 + e] = wv;
+            ow[e] = __float_as_uint(wv);
+        }
+        const uint4 line = j < 7 ? make_uint4(ow[0], ow[1], ow[2], ow[3])
+                                 : make_uint4(ow[0], ow[1], flag, flag);
+#pragma unroll
+        for (int k = 1; k < WORLD; ++k)
+            st_ll(tx((rank + k) % WORLD) + (RL + ln) * 8 + j, line);
+    }
+
+    // C: receive every peer's updated block into our w.
+#pragma unroll 1
+    for (int k = 1; ok && k < WORLD; ++k) {
+        const int q = (rank + k) % WORLD;
+        uint64_t oq, lq;
+        shard(q, oq, lq);
+        const uint64_t nb = lq * 4, nl = (nb + 119) / 120;
+        float *base = wloc + oq;
+        for (uint64_t ln = g0; ln < nl; ln += groups) {
+            uint4 *src = rx(q) + (RL + ln) * 8 + j;
+            const uint4 r = ll128_wait(src, flag, gmask, p, ok);
+            if (!ok) {
+                if (j == 0) report_timeout(p.err, 2, q, vr);
+                break;
+            }
+            st_ll(src, make_uint4(0u, 0u, 0u, 0u));
+            const uint64_t pr = 15 * ln + 2 * j;
+            store_pair(base, pr, nb, make_uint2(r.x, r.y));
+            if (j < 7) store_pair(base, pr + 1, nb, make_uint2(r.z, r.w));
+        }
+    }
+
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&mine->arrive, 1u);
+        s_last = (prev == gridDim.x - 1);
+        if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        mine->arrive = 0;
+        mine->calls += 1;
+        mine->ll_calls += 1;
+        mine->epoch = epoch;
+        if (p.done[vr] != nullptr) *p.done[vr] = epoch;
+    }
+}
+
+namespace {
 template <typename TG, int MODE>
 KernelFnLL pick_ll_sgd_m(int world) {
     switch (world) {
@@ -1495,10 +1666,32 @@ bool ll_sgd_fits(uint64_t blk, int dtype, int mode, uint64_t ll_pairs) {
     return (blk * sg + 7) / 8 + (blk * sw + 7) / 8 <= ll_pairs;
 }
 
+namespace {
+KernelFnLL pick_ll128_sgd(int world) {
+    switch (world) {
+        case 2: return gdraa_ll128_sgd_kernel<2>;
+        case 3: return gdraa_ll128_sgd_kernel<3>;
+        case 4: return gdraa_ll128_sgd_kernel<4>;
+        case 5: return gdraa_ll128_sgd_kernel<5>;
+        case 6: return gdraa_ll128_sgd_kernel<6>;
+        case 7: return gdraa_ll128_sgd_kernel<7>;
+        case 8: return gdraa_ll128_sgd_kernel<8>;
+        default: return nullptr;
+    }
+}
+}  // namespace
+
 cudaError_t launch_gdraa_ll_sgd(const KParams &p, int dtype, int mode, int vr_rows,
                                 bool cooperative, cudaStream_t s) {
     KernelFnLL fn = nullptr;
-    if (mode == kSgd)
+    // LL128 lines for fp32 gradients + fp32 w (same size rule as the mean), when the two
+    // line regions fit the slot from its first 128-byte boundary
+    const uint64_t rl = (p.blk * 4 + 119) / 120;
+    const bool l128 = dtype == GDRAA_F32 && mode == kSgd && ll128_for(p.n * 4, p.world) &&
+                      128 + 2 * rl * 128 <= 16 * p.ll_pairs;
+    if (l128)
+        fn = pick_ll128_sgd(p.world);
+    else if (mode == kSgd)
         fn = dtype == GDRAA_F32 ? pick_ll_sgd_m<float, kSgd>(p.world)
                                 : pick_ll_sgd_m<__nv_bfloat16, kSgd>(p.world);
     else if (mode == kSgdMp)
@@ -1516,8 +1709,9 @@ cudaError_t launch_gdraa_ll_sgd(const KParams &p, int dtype, int mode, int vr_ro
     if (e != cudaSuccess) return e;
     // every CTA polls entries other CTAs (and peers) produce: the grid must be resident
     const uint64_t es = dtype == GDRAA_F32 ? 4 : 2;
-    const uint64_t work = (p.blk * es + 7) / 8 > (p.blk + E - 1) / E ? (p.blk * es + 7) / 8
-                                                                       : (p.blk + E - 1) / E;
+    const uint64_t work = l128 ? rl * 8
+                               : ((p.blk * es + 7) / 8 > (p.blk + E - 1) / E ? (p.blk * es + 7) / 8
+                                                                             : (p.blk + E - 1) / E);
     uint64_t gx = (work + kT - 1) / kT;
     const uint64_t cap = static_cast<uint64_t>(sms) * per_sm / vr_rows;
     if (gx > cap) gx = cap;

@@ -7,6 +7,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import oracle  # noqa: E402
@@ -38,9 +39,33 @@ def main():
                             compare(from_dev(bufs[r]), exp, dt,
                                     what=f"ll128 mean N={N} {dt} L={L} {fam} r{r}")
                         count += 1
-    # LL128 mean calls interleaved with small-message SGD steps (LL format) on the same
-    # receive slots: each result must still be the oracle's
+    # the LL128 form of the small-message SGD step (fp32 g, fp32 w, with weight decay)
     import synth
+    for N in range(2, 9):
+        lim = gdraa.gdraa_small_step_bytes(N) // 4
+        for i, L in enumerate([1, 29, 30, 31, 61, 64 * N + 1, 257, 4097, 70_001, lim]):
+            gs = make_grads("like" if i % 2 else "int", 700 + 10 * N + i, N, L, False)
+            w0, v0 = synth.w_like(700 + N, L), synth.w_like(701 + N, L)
+            w_exp, v_exp = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, 0.001)
+            g_d = [to_dev(g) for g in gs]
+            w_d = [to_dev(w0) for _ in range(N)]
+            v_d = [to_dev(v0) for _ in range(N)]
+            gdraa.gdraa_vr_sgd_step_ex(w_d, g_d, v_d, 0.1, 0.9, 0.001)
+            torch.cuda.synchronize()
+            for r in range(N):
+                off, ln = gdraa.gdraa_shard(N, r, L)
+                compare(from_dev(w_d[r]), w_exp, "f32", what=f"ll128 sgd w N={N} L={L} r{r}")
+                compare(from_dev(v_d[r])[off:off + ln], v_exp[off:off + ln], "f32",
+                        what=f"ll128 sgd v N={N} L={L} r{r}")
+                outside = np.concatenate([from_dev(v_d[r])[:off], from_dev(v_d[r])[off + ln:]])
+                assert np.array_equal(outside.view(np.uint32), np.concatenate(
+                    [v0[:off], v0[off + ln:]]).view(np.uint32)), "v outside the shard"
+                assert np.array_equal(from_dev(g_d[r]).view(np.uint32), gs[r].view(np.uint32))
+            count += 1
+
+    # LL128 mean calls interleaved with small-message SGD steps on the same
+    # receive slots (fp32 steps: LL128 lines, the bf16 step: LL entries): each result must
+    # still be the oracle's
     for N in (2, 3, 4, 8):
         L = 4097
         w0, v0 = synth.w_like(950 + N, L), synth.w_like(951 + N, L)
@@ -48,7 +73,8 @@ def main():
         v_d = [to_dev(v0) for _ in range(N)]
         w_ref, v_ref = w0.copy(), v0.copy()
         for step in range(6):
-            gs = make_grads("like", 960 + 10 * N + step, N, L, False)
+            bf = step == 3   # one step with bf16 gradients: LL entries, not LL128 lines
+            gs = make_grads("like", 960 + 10 * N + step, N, L, bf)
             if step % 2 == 0:
                 bufs = [to_dev(g) for g in gs]
                 gdraa.gdraa_vr_allreduce_mean(bufs)
@@ -57,7 +83,7 @@ def main():
                 for r in range(N):
                     compare(from_dev(bufs[r]), exp, "f32", what=f"mixed mean N={N} s{step} r{r}")
             else:
-                g_d = [to_dev(g) for g in gs]
+                g_d = [to_dev(g, bf) for g in gs]
                 gdraa.gdraa_vr_sgd_step(w_d, g_d, v_d, 0.1, 0.9)
                 torch.cuda.synchronize()
                 w_ref, v_new = oracle.sgd_step(gs, w_ref, v_ref, 0.1, 0.9)
