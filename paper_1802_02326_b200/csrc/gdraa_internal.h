@@ -97,9 +97,11 @@ cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool coope
 // Whether launch_gdraa_ll uses the LL128 line format for a call of nbytes per rank:
 // from kLL128MinBytes / (N-1) up (measured crossover); GDRAA_LL128=1 / 0 forces it
 // on / off (ll128_mode: 1 / 0; 2 = by size).  Read once per process.
+// min_bytes: the threshold for n * s * (N-1) (0: kLL128MinBytes, the mean's).
 int ll128_mode();
-bool ll128_for(uint64_t nbytes, int world);
-constexpr uint64_t kLL128MinBytes = 512ull << 10;
+bool ll128_for(uint64_t nbytes, int world, uint64_t min_bytes = 0);
+constexpr uint64_t kLL128MinBytes = 512ull << 10;      // small-message mean
+constexpr uint64_t kLL128SgdMinBytes = 3ull << 20;     // small-message SGD step (fp32)
 
 // Small-message fused SGD step (kSgd / kSgdMp): gradient blocks and updated blocks travel
 // as LL entries through the same receive areas; the data carries both synchronisations.

@@ -1434,9 +1434,10 @@ int ll128_mode() {
     return v;
 }
 
-bool ll128_for(uint64_t nbytes, int world) {
+bool ll128_for(uint64_t nbytes, int world, uint64_t min_bytes) {
     const int m = ll128_mode();
     if (m != 2) return m == 1;
+    if (min_bytes != 0) return nbytes * static_cast<uint64_t>(world - 1) >= min_bytes;
     // measured crossover (profiles/r48_sweep_n*_ll128_*.jsonl): the line format wins from
     // ~512 KiB at N = 2 and ~256 KiB at N = 4, where LL's 2x bytes dominate; below, the
     // LL entries' shorter poll path wins by <= 0.8 us
@@ -1684,10 +1685,13 @@ KernelFnLL pick_ll128_sgd(int world) {
 cudaError_t launch_gdraa_ll_sgd(const KParams &p, int dtype, int mode, int vr_rows,
                                 bool cooperative, cudaStream_t s) {
     KernelFnLL fn = nullptr;
-    // LL128 lines for fp32 gradients + fp32 w (same size rule as the mean), when the two
-    // line regions fit the slot from its first 128-byte boundary
+    // LL128 lines for fp32 gradients + fp32 w from n * 4 * (N-1) >= 3 MiB (measured at
+    // N = 2, profiles/r50_sweep_sgd_n2_ll128_*.jsonl: 1.18x at 4 MiB = config 1, 0.92-0.95x
+    // from 1 KiB to 2 MiB), when the two line regions fit the slot past its first
+    // 128-byte boundary
     const uint64_t rl = (p.blk * 4 + 119) / 120;
-    const bool l128 = dtype == GDRAA_F32 && mode == kSgd && ll128_for(p.n * 4, p.world) &&
+    const bool l128 = dtype == GDRAA_F32 && mode == kSgd &&
+                      ll128_for(p.n * 4, p.world, kLL128SgdMinBytes) &&
                       128 + 2 * rl * 128 <= 16 * p.ll_pairs;
     if (l128)
         fn = pick_ll128_sgd(p.world);
