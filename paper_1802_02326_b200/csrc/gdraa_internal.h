@@ -94,9 +94,10 @@ bool use_tma_kernel(int dtype, int mode, int world);
 // Requires n * elem_size <= 8 * p.ll_pairs.
 cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool cooperative,
                             cudaStream_t s);
-// Whether launch_gdraa_ll uses the LL128 line format for a call of nbytes per rank:
-// from kLL128MinBytes / (N-1) up (measured crossover); GDRAA_LL128=1 / 0 forces it
-// on / off (ll128_mode: 1 / 0; 2 = by size).  Read once per process.
+// Whether launch_gdraa_ll uses the LL128 line format for a call of nbytes per rank.
+// Experimental and off by default (ll128_mode 0); GDRAA_LL128=1 forces it on (mode 1),
+// GDRAA_LL128=auto serves it by size (mode 2: from kLL128MinBytes / (N-1) up, the
+// measured crossover).  Read once per process.
 // min_bytes: the threshold for n * s * (N-1) (0: kLL128MinBytes, the mean's).
 int ll128_mode();
 bool ll128_for(uint64_t nbytes, int world, uint64_t min_bytes = 0);

@@ -1427,9 +1427,13 @@ cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows, boo
 
 int ll128_mode() {
     static const int v = [] {
+        // experimental, off unless asked for: GDRAA_LL128=1 (always) or =auto (by size).
+        // A virtual-rank SGD parity test failed once with the SGD form served by size
+        // (profiles/r51_pytest_gpu_n4.log) after passing twice; until that is understood
+        // neither LL128 kernel is on the default path.
         const char *e = std::getenv("GDRAA_LL128");
-        if (e == nullptr || *e == 0) return 2;
-        return e[0] == '1' ? 1 : e[0] == '0' ? 0 : 2;
+        if (e == nullptr || *e == 0) return 0;
+        return e[0] == '1' ? 1 : e[0] == 'a' ? 2 : 0;
     }();
     return v;
 }
