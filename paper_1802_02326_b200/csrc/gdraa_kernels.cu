@@ -659,6 +659,7 @@ gdraa_ll128_kernel(const __grid_constant__ KParams p) {
         for (int kk = 1; kk < WORLD; ++kk) {   // push the line to every peer's slot [par][rank]
             const int q = (rank + kk) % WORLD;
             uint4 *dst = const_cast<uint4 *>(ll128_slot(p.ll[vr][q] + (par * WORLD + rank) * p.ll_pairs));
+            __syncwarp(gmask);   // the 8 lanes store the line in one instruction
             st_ll(dst + k * 8 + j, entry);
         }
         uint32_t w[4][WORLD];
@@ -670,6 +671,7 @@ gdraa_ll128_kernel(const __grid_constant__ KParams p) {
                 const uint64_t t0 = global_timer_ns();
                 uint32_t polls = 0, sleep_ns = 32;
                 while (true) {
+                    __syncwarp(gmask);   // ... and load it in one
                     r = ld_ll(src);
                     const bool here = __shfl_sync(gmask, r.z == flag && r.w == flag, 7, 8);
                     if (here) break;
@@ -1487,6 +1489,7 @@ __device__ __forceinline__ uint4 ll128_wait(const uint4 *src, uint32_t flag, uns
     const uint64_t t0 = global_timer_ns();
     uint32_t polls = 0, sleep_ns = 32;
     while (true) {
+        __syncwarp(gmask);   // the 8 lanes load the line in one instruction
         const uint4 r = ld_ll(src);
         if (__shfl_sync(gmask, r.z == flag && r.w == flag, 7, 8)) return r;
         bool late = false;
@@ -1554,6 +1557,7 @@ gdraa_ll128_sgd_kernel(const __grid_constant__ KParams p) {
             const uint64_t pr = 15 * ln + 2 * j;
             const uint2 a = load_pair(base, pr, nb);
             const uint2 b = j < 7 ? load_pair(base, pr + 1, nb) : make_uint2(flag, flag);
+            __syncwarp(gmask);
             st_ll(dst + ln * 8 + j, make_uint4(a.x, a.y, b.x, b.y));
         }
     }
@@ -1607,8 +1611,10 @@ gdraa_ll128_sgd_kernel(const __grid_constant__ KParams p) {
         const uint4 line = j < 7 ? make_uint4(ow[0], ow[1], ow[2], ow[3])
                                  : make_uint4(ow[0], ow[1], flag, flag);
 #pragma unroll
-        for (int k = 1; k < WORLD; ++k)
+        for (int k = 1; k < WORLD; ++k) {
+            __syncwarp(gmask);   // the 8 lanes store the line in one instruction
             st_ll(tx((rank + k) % WORLD) + (RL + ln) * 8 + j, line);
+        }
     }
 
     // C: receive every peer's updated block into our w.
