@@ -2,7 +2,7 @@
 LL-format small-message SGD steps, then LL128 steps (GDRAA_LL128=auto must be set), and
 every mismatch with the oracle is mapped to (block owner, line, lane, element in lane).
 
-    GDRAA_LL128=auto python tools/ll128_diag.py [N=4] [tries=5]
+    GDRAA_LL128=auto python tools/ll128_diag.py [N=4] [tries=5] [--full]
 """
 import json
 import os
@@ -21,12 +21,16 @@ from paper_1802_02326_b200 import gdraa  # noqa: E402
 
 def main():
     assert os.environ.get("GDRAA_LL128") == "auto"
-    N = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-    tries = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    N = int(args[0]) if args else 4
+    tries = int(args[1]) if len(args) > 1 else 5
     lim = gdraa.gdraa_small_step_bytes(N) // 4
     dev = "cuda:0"
     for t in range(tries):
-        seq = [65_537] * 3 + [lim - 1] * 3
+        # the failing test's exact sequence (tests/test_gpu_parity.py::
+        # test_vr_sgd_latency_path): every size 3 times, LL-format up to 65537
+        sizes = [1, 3, 63, 65, 127, 4097, 65_537] if "--full" in sys.argv else [65_537]
+        seq = [L for L in sizes for _ in range(3)] + [lim - 1] * 3
         w = synth.w_like(901 + t, 1)  # placeholder, reset per size below
         size_prev = None
         for step, L in enumerate(seq):
@@ -35,11 +39,13 @@ def main():
                 w_d = [torch.from_numpy(w).to(dev) for _ in range(N)]
                 v_d = [torch.from_numpy(v).to(dev) for _ in range(N)]
                 size_prev = L
-            gs = [synth.grad_like(910 + 7 * t + step, p, L) for p in range(N)]
+            it = step % 3
+            from tests.test_gpu_parity import make_grads
+            gs = make_grads("like", (900 + L % 13) if it == 0 else (910 + it), N, L, False)
             g_d = [torch.from_numpy(g).to(dev) for g in gs]
-            gdraa.gdraa_vr_sgd_step(w_d, g_d, v_d, 0.1, 0.9)
+            gdraa.gdraa_vr_sgd_step_ex(w_d, g_d, v_d, 0.1, 0.9, 0.001)
             torch.cuda.synchronize()
-            w, v_new = oracle.sgd_step(gs, w, v, 0.1, 0.9)
+            w, v_new = oracle.sgd_step_wd(gs, w, v, 0.1, 0.9, 0.001)
             blk = gdraa.gdraa_shard(N, 0, L)[1]
             out = {"try": t, "step": step, "L": L, "path": "ll128" if L == lim - 1 else "ll"}
             for r in range(N):
