@@ -15,7 +15,9 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/ll128_probe \
 //        tools/ll128_probe.cu
-//   tools/ll128_probe [lines_per_epoch=262144] [epochs=200] [control=0]
+//   tools/ll128_probe [lines_per_epoch=262144] [epochs=200] [control=0] [same=0]
+// same = 1: sender and receiver on GPU 0 (half the SMs each), the buffer in GPU 0's own
+// memory -- the virtual-rank case, where no NVLink is involved.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -163,19 +165,22 @@ int main(int argc, char **argv) {
     const uint64_t lines = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 262144;
     const int epochs = argc > 2 ? std::atoi(argv[2]) : 200;
     const int control = argc > 3 ? std::atoi(argv[3]) : 0;
+    const int same = argc > 4 ? std::atoi(argv[4]) : 0;
+    const int dr = same ? 0 : 1;   // the receiver's (and the buffer's) device
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
-    if (ndev < 2) {
+    if (ndev < 2 && !same) {
         std::printf("{\"error\": \"needs 2 GPUs\"}\n");
         return 1;
     }
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int grid = same ? sms / 2 : sms;
     uint64_t *buf = nullptr, *ack = nullptr;
     unsigned *arrive = nullptr, *gave_up_s = nullptr, *gave_up_r = nullptr;
     unsigned long long *torn = nullptr, *polls = nullptr;
-    CK(cudaSetDevice(1));
-    CK(cudaDeviceEnablePeerAccess(0, 0));
+    CK(cudaSetDevice(dr));
+    if (!same) CK(cudaDeviceEnablePeerAccess(0, 0));
     CK(cudaMalloc(&buf, lines * 128));
     CK(cudaMemset(buf, 0, lines * 128));
     CK(cudaMalloc(&arrive, 2 * sizeof(unsigned)));
@@ -186,7 +191,7 @@ int main(int argc, char **argv) {
     polls = torn + 1;
     CK(cudaDeviceSynchronize());
     CK(cudaSetDevice(0));
-    CK(cudaDeviceEnablePeerAccess(1, 0));
+    if (!same) CK(cudaDeviceEnablePeerAccess(1, 0));
     CK(cudaMalloc(&ack, 2 * sizeof(uint64_t)));
     CK(cudaMemset(ack, 0, 2 * sizeof(uint64_t)));
     gave_up_s = reinterpret_cast<unsigned *>(ack + 1);
@@ -196,16 +201,20 @@ int main(int argc, char **argv) {
     cudaEvent_t t0, t1;
     CK(cudaEventCreate(&t0));
     CK(cudaEventCreate(&t1));
-    CK(cudaSetDevice(1));
-    receiver<<<sms, 256>>>(buf, lines, epochs, ack, arrive, torn, polls, gave_up_r);
+    cudaStream_t rs;   // same device: the two grids need separate streams to run together
+    CK(cudaSetDevice(dr));
+    CK(cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking));
+    receiver<<<grid, 256, 0, rs>>>(buf, lines, epochs, ack, arrive, torn, polls, gave_up_r);
     CK(cudaGetLastError());
     CK(cudaSetDevice(0));
-    CK(cudaEventRecord(t0));
-    sender<<<sms, 256>>>(buf, lines, epochs, ack, gave_up_s, control);
+    cudaStream_t ss;
+    CK(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
+    CK(cudaEventRecord(t0, ss));
+    sender<<<grid, 256, 0, ss>>>(buf, lines, epochs, ack, gave_up_s, control);
     CK(cudaGetLastError());
-    CK(cudaEventRecord(t1));
+    CK(cudaEventRecord(t1, ss));
     CK(cudaDeviceSynchronize());
-    CK(cudaSetDevice(1));
+    CK(cudaSetDevice(dr));
     CK(cudaDeviceSynchronize());
     unsigned long long h[2];
     CK(cudaMemcpy(h, torn, sizeof h, cudaMemcpyDeviceToHost));
@@ -213,14 +222,16 @@ int main(int argc, char **argv) {
     CK(cudaMemcpy(&gu[1], gave_up_r, sizeof(unsigned), cudaMemcpyDeviceToHost));
     CK(cudaSetDevice(0));
     CK(cudaMemcpy(&gu[0], gave_up_s, sizeof(unsigned), cudaMemcpyDeviceToHost));
+    uint64_t acked = 0;
+    CK(cudaMemcpy(&acked, ack, sizeof acked, cudaMemcpyDeviceToHost));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, t0, t1));
     const double bytes = static_cast<double>(lines) * 128 * epochs;
-    std::printf("{\"probe\": \"ll128_line_atomicity\", \"control\": %d, \"lines_per_epoch\": %llu, \"epochs\": %d, "
+    std::printf("{\"probe\": \"ll128_line_atomicity\", \"same_device\": %d, \"control\": %d, \"lines_per_epoch\": %llu, \"epochs\": %d, "
                 "\"lines_checked\": %.0f, \"torn_lines\": %llu, \"polls\": %llu, "
-                "\"sender_ms\": %.3f, \"gbs_one_way_incl_acks\": %.1f, \"gave_up\": [%u, %u]}\n",
-                control, static_cast<unsigned long long>(lines), epochs,
+                "\"sender_ms\": %.3f, \"gbs_one_way_incl_acks\": %.1f, \"gave_up\": [%u, %u], \"acked_epochs\": %llu}\n",
+                same, control, static_cast<unsigned long long>(lines), epochs,
                 static_cast<double>(lines) * epochs, h[0], h[1], ms, bytes / (ms * 1e-3) / 1e9, gu[0],
-                gu[1]);
+                gu[1], static_cast<unsigned long long>(acked));
     return 0;
 }
