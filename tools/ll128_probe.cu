@@ -197,6 +197,11 @@ int main(int argc, char **argv) {
     gave_up_s = reinterpret_cast<unsigned *>(ack + 1);
     CK(cudaDeviceSynchronize());
 
+    // load both kernels now: under lazy module loading the first launch of a kernel waits
+    // for the device to idle, which on one device deadlocks the second grid behind the first
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, sender));
+    CK(cudaFuncGetAttributes(&fa, receiver));
     // both grids must be fully resident (they wait on each other): one CTA per SM
     cudaEvent_t t0, t1;
     CK(cudaEventCreate(&t0));
