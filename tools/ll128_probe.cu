@@ -2,7 +2,8 @@
 // arrive over NVLink as a unit, so that a flag in the line's last 8 bytes implies the other
 // 120 bytes are there too?  That is the premise of an "LL128" small-message protocol
 // (15/16 payload per line instead of the LL path's 1/2, DESIGN.md §6 latency path), which
-// the library does NOT use; this probe measures the premise before anything relies on it.
+// the library serves only experimentally (GDRAA_LL128, off by default); this probe
+// measures the premise the experimental kernels rest on.
 //
 // Two devices, one process.  The sender (GPU 0) writes, for epochs e = 1..E, a buffer of
 // LINES 128-byte lines into GPU 1's memory: lane j of each 8-lane group stores 16 bytes
