@@ -143,8 +143,9 @@ class OracleSample:
             self.gs = [synth.to_bf16_bits_trunc(g) for g in self.gs]
         self.w, self.v = synth.w_like(0, self.n), np.zeros(self.n, np.float32)
         s_g = 2 if g_dt == "bf16" else 4
-        # the metric's bytes for this sample, summed over ranks as `value` is
-        self.bytes = algorithmic_bytes(self.n, N, s_g, 2 if mp else 4) * N
+        # the metric's per-rank bytes for one step of this sample (as `value`: one step of
+        # all N ranks takes the measured time, so per-rank bytes / that time)
+        self.bytes = algorithmic_bytes(self.n, N, s_g, 2 if mp else 4)
 
     def step(self):
         t0 = time.perf_counter()
@@ -230,12 +231,63 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config_dict(args, L, g_dt, desc, N, "oracle (CPU)"),
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model(),
+                         "host_cores": os.cpu_count()},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), file=OUT, flush=True)
     return 0
+
+
+def free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as t:
+        t.bind(("127.0.0.1", 0))
+        return t.getsockname()[1]
+
+
+def self_launch(n, argv):
+    """Re-run this script as N ranks under torch.distributed.run (one process per GPU,
+    NCCL plumbing, rendezvous on 127.0.0.1).  Every rank sends library output to stderr;
+    rank 0 alone prints the JSON line, on the stdout inherited from this process."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           os.path.join(ROOT, "bench.py"), *argv]
+    return subprocess.run(cmd, cwd=ROOT).returncode
+
+
+def dry_launch(args):
+    """The launch path alone (CPU test of self_launch): N ranks meet in a gloo group;
+    rank 0 prints what every rank saw."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    me = {"rank": rank, "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
+          "master_addr": os.environ.get("MASTER_ADDR")}
+    table = [me]
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        table = [None] * world
+        dist.all_gather_object(table, me)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_launch": True, "n_gpus": args.gpus, "world": world,
+                          "ranks": table}), file=OUT, flush=True)
+    return 0
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or None
 
 
 def config_dict(args, L, g_dt, desc, N, path=None):
@@ -275,7 +327,14 @@ def main():
                          "replay of them (the default: host launch cost out of the step)")
     ap.add_argument("--graph", dest="graph", action="store_true")
     ap.set_defaults(graph=True)
+    ap.add_argument("--dry-launch", action="store_true",
+                    help="check the process launch only: every rank joins a gloo group, rank "
+                         "0 prints the rank table as the JSON line (no GPU work)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # `python bench.py --gpus N` without a launcher: start the N ranks ourselves
+        # (torchrun on a free loopback port); rank 0's JSON line reaches our stdout.
+        return self_launch(args.gpus, sys.argv[1:])
     # Exactly one JSON line on stdout: anything libraries print (NCCL banners, ...) goes
     # to stderr; the result line goes to the saved stdout.
     global OUT
@@ -283,6 +342,8 @@ def main():
     os.dup2(2, 1)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.dry_launch:
+        return dry_launch(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -407,8 +468,11 @@ def main():
         launches = graph_launches
     ms_step = ms / args.steps
     per_rank = algorithmic_bytes(L, N, s_g, s_w)
-    value = per_rank * N / (ms_step * 1e-3) / 1e9           # whole job
     achieved = per_rank / (ms_step * 1e-3) / 1e9            # per rank = per launch
+    job_total = per_rank * N / (ms_step * 1e-3) / 1e9       # summed over ranks
+    # the metric is bus GB/s (NCCL's busBW convention): B_nv / t per rank;
+    # N = 1 has no bus and reports the launch's HBM rate
+    value = achieved
 
     # ---- per-call distribution (untimed pass; an event pair around every call) ----
     M = min(args.steps, 200)
@@ -485,7 +549,7 @@ def main():
         t = torch.tensor([ems], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ems = float(t.item())
-    e2e_val = per_rank * N / (ems / args.e2e_steps * 1e-3) / 1e9
+    e2e_val = per_rank / (ems / args.e2e_steps * 1e-3) / 1e9   # same definition as value
 
     # the same per-step copies alone (H2D and D2H concurrently, no step): the PCIe bound
     # the e2e figure is held to
@@ -508,7 +572,7 @@ def main():
         t = torch.tensor([cms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         cms = float(t.item())
-    copy_bound = per_rank * N / (cms / args.e2e_steps * 1e-3) / 1e9
+    copy_bound = per_rank / (cms / args.e2e_steps * 1e-3) / 1e9
 
     # ---- NCCL all_reduce(AVG) of the same gradient buffer (reference point) ----
     nccl = None
@@ -556,7 +620,7 @@ def main():
         if N == 1 and not args.no_cpu_baseline:
             cv, sample, _ = oracle_baseline(L, N, g_dt, 10.0, mp)
             cpu = {"value": cv / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                   "sample": sample}
+                   "sample": sample, "cpu_model": cpu_model(), "host_cores": os.cpu_count()}
             mv, k, mreps, mn = oracle_baseline_mt(L, N, g_dt, 5.0, mp)
             cpu["threaded_variant"] = {
                 "value": mv / 1e9, "unit": "GB/s", "cores": k,
@@ -569,10 +633,13 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": config_dict(args, L, g_dt, desc, N, path),
-            "value_definition": ("sum over ranks of per-rank algorithmic bytes / step time; "
+            "value_definition": ("per-rank algorithmic bytes of one step / step time (max "
+                                 "over ranks); "
                                  + (f"N=1: HBM bytes {per_rank / L:g}*L" if N == 1 else
-                                    f"N>=2: NVLink bus bytes (N-1)/N*L*({s_g}+{s_w}) per rank")),
+                                    f"N>=2: bus bytes B_nv = (N-1)/N*L*({s_g}+{s_w}) per rank "
+                                    "per direction (NCCL busBW convention)")),
             "bus_gbs_per_rank": achieved if N > 1 else 0.0,
+            "job_total_gbs": job_total,
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "GB/s", "steps": args.e2e_steps,
                     "h2d_bytes_per_step": L * s_g * N, "d2h_bytes_per_step": L * s_w,

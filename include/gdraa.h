@@ -26,8 +26,13 @@
  *    never arrives within GDRAA_TIMEOUT_MS, default 30000) are STICKY: the next call and
  *    gdraa_finalize return GDRAA_ETIMEOUT and gdraa_last_error() names the missing ranks.
  *  - Collective calls (init, register, allreduce_mean, sgd_step, finalize) must be
- *    issued in the same order with the same sizes on every rank, one outstanding
- *    collective per process ("same iteration number and same L").
+ *    issued in the same order with the same sizes on every rank ("same iteration
+ *    number and same L").  Calls on one stream run back to back; a call issued on a
+ *    different stream than the previous call is ordered after all work issued so far
+ *    on that previous stream (an event the library records there and waits on), so
+ *    collectives never overlap on the device.  The previous call's stream must still
+ *    exist when such a call is made.  Inside a CUDA-graph capture this ordering is the
+ *    graph's (the library adds no cross-stream edge to a capturing stream).
  *  - The caller owns every data buffer and keeps it allocated until gdraa_finalize.
  *    The library owns its signal pads, peer mappings and host-mapped flag pages.
  */
@@ -236,6 +241,11 @@ typedef struct {
                                   gdraa_small_message_bytes, sgd_step below
                                   gdraa_small_step_bytes), whose synchronisation travels
                                   with the data (no device barrier; not in sync_waits)       */
+    uint64_t iter_done;        /* this rank's "IterDone" flag as the job server sees
+                                  it in the shared go/done page: written by the last CTA of
+                                  every call's kernel = device calls completed             */
+    uint64_t iter_start;       /* this rank's "IterStart" flag in the same page (gated mode
+                                  launches call e only once it reads >= e)                 */
 } gdraa_stats_t;
 
 /*
@@ -279,6 +289,25 @@ int gdraa_vr_sgd_step_ex(int world, float *const *w, const void *const *g, float
 int gdraa_vr_sgd_step_mp(int world, float *const *w_master, void *const *w_model,
                          const void *const *g, float *const *v, size_t n, int dtype, float lr,
                          float mom, float wd, gdraa_stream_t s);
+
+/*
+ * Bucketed virtual-rank calls (NEXT-3 on one GPU): the calls above on the element
+ * range [first, first + count) of every rank's n-element buffers, with the range's own
+ * owner partition (rank r owns [first + off_r, +len_r), off_r/len_r = gdraa_shard(world,
+ * r, count)) -- exactly the semantics of gdraa_allreduce_mean_range / gdraa_sgd_step_range
+ * / gdraa_sgd_step_mp_range, so the per-range owner rule is testable on one GPU.
+ *   first: multiple of 8; count >= 1; first + count <= n.  Other arguments as above.
+ * Errors: EINVAL (bad range, null arrays), ECUDA, ETIMEOUT (returned by a later call).
+ */
+int gdraa_vr_allreduce_mean_range(int world, void *const *bufs, size_t n, int dtype,
+                                  size_t first, size_t count, gdraa_stream_t s);
+int gdraa_vr_sgd_step_range(int world, float *const *w, const void *const *g, float *const *v,
+                            size_t n, int dtype, size_t first, size_t count, float lr, float mom,
+                            float wd, gdraa_stream_t s);
+int gdraa_vr_sgd_step_mp_range(int world, float *const *w_master, void *const *w_model,
+                               const void *const *g, float *const *v, size_t n, int dtype,
+                               size_t first, size_t count, float lr, float mom, float wd,
+                               gdraa_stream_t s);
 
 #ifdef __cplusplus
 }

@@ -65,6 +65,7 @@ struct KParams {
     volatile uint64_t *done[kMaxWorld];      // host-mapped done flags (device alias) or null
     const volatile int32_t *abort;           // host-mapped job-server abort flag, or null:
                                              // spins give up early once a rank has died
+    uint32_t flags;                          // kFlag* bits (launch-variant switches)
 #ifdef GDRAA_TRACE
     uint64_t *trace;                         // tools/tune.cu only: %globaltimer stamps
 #endif
@@ -73,6 +74,11 @@ struct KParams {
 // kMean: dst = mean (allreduce_mean).  kSgd: dst = w' (fp32, replicated w).
 // kSgdMp: fp32 master w sharded like v (p.wm), dst = bf16 RNE(w') model copy (NEXT-1).
 enum Mode { kMean = 0, kSgd = 1, kSgdMp = 2 };
+
+// KParams::flags.  kFlagCtaFence: at exit, one fence.acq_rel.sys per CTA after
+// __syncthreads() instead of one per thread (GDRAA_EXIT_FENCE=cta|thread).
+constexpr uint32_t kFlagCtaFence = 1u;
+uint32_t env_kernel_flags();
 constexpr int kModes = 3;
 
 // Launch the fused kernel.  grid_x CTAs per (virtual) rank; vr_rows = gridDim.y.
@@ -94,16 +100,6 @@ bool use_tma_kernel(int dtype, int mode, int world);
 // Requires n * elem_size <= 8 * p.ll_pairs.
 cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool cooperative,
                             cudaStream_t s);
-// Whether launch_gdraa_ll uses the LL128 line format for a call of nbytes per rank.
-// Experimental and off by default (ll128_mode 0); GDRAA_LL128=1 forces it on (mode 1),
-// GDRAA_LL128=auto serves it by size (mode 2: from kLL128MinBytes / (N-1) up, the
-// measured crossover).  Read once per process.
-// min_bytes: the threshold for n * s * (N-1) (0: kLL128MinBytes, the mean's).
-int ll128_mode();
-bool ll128_for(uint64_t nbytes, int world, uint64_t min_bytes = 0);
-constexpr uint64_t kLL128MinBytes = 512ull << 10;      // small-message mean
-constexpr uint64_t kLL128SgdMinBytes = 3ull << 20;     // small-message SGD step (fp32)
-
 // Small-message fused SGD step (kSgd / kSgdMp): gradient blocks and updated blocks travel
 // as LL entries through the same receive areas; the data carries both synchronisations.
 // Requires ll_sgd_fits(p.blk, ...).

@@ -416,9 +416,15 @@ gdraa_kernel(const __grid_constant__ KParams p) {
     // Let the next kernel on the stream start launching; it waits for our completion
     // (griddepcontrol.wait above) before touching anything.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (WORLD > 1) fence_acq_rel_sys();   // N = 1: the kernel boundary orders our stores
+    // Our pushes must be performed system-wide before the peers hear of them.  Either
+    // every thread fences its own stores, or (kFlagCtaFence) the CTA synchronises and
+    // one thread fences for all of them (release cumulativity over bar.sync).
+    // N = 1: the kernel boundary orders our stores.
+    const bool cta_fence = (p.flags & kFlagCtaFence) != 0;
+    if (WORLD > 1 && !cta_fence) fence_acq_rel_sys();
     __syncthreads();
     if (threadIdx.x == 0) {
+        if (WORLD > 1 && cta_fence) fence_acq_rel_sys();
         const unsigned prev = atomicAdd(&mine->arrive, 1u);
         s_last = (prev == gridDim.x - 1);
         if (s_last) __threadfence();
@@ -595,119 +601,6 @@ gdraa_ll_kernel(const __grid_constant__ KParams p) {
         if (!ok) break;
         store_pair(buf, j, nbytes,
                    make_uint2(WordMean<TG, WORLD>::run(w0), WordMean<TG, WORLD>::run(w1)));
-    }
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned prev = atomicAdd(&mine->arrive, 1u);
-        s_last = (prev == gridDim.x - 1);
-        if (s_last) __threadfence();
-    }
-    __syncthreads();
-    if (s_last && threadIdx.x == 0) {
-        mine->arrive = 0;
-        mine->calls += 1;
-        mine->ll_calls += 1;
-        mine->epoch = epoch;
-        if (p.done[vr] != nullptr) *p.done[vr] = epoch;
-    }
-}
-
-// ---------------------------------------------------------------------------------
-// LL128 variant of the small-message allreduce_mean (served when n * s * (N-1) >= 512 KiB;
-// GDRAA_LL128=1 / 0 forces it on / off and must match on every rank, checked at init).  Same receive slots, same parity rule, same fold;
-// the slot is used as 128-byte lines of 120 payload bytes + an 8-byte flag {flag, flag}
-// instead of 16-byte entries of 8 payload bytes + two flags.  Lane j (0..7) of an 8-lane
-// group owns bytes [16j, 16j+16) of one line and stores / loads them with one 16-byte
-// access, so each line moves in one warp instruction; lane 7 carries the flag.  A flag
-// seen implies the whole line is there only because NVLink delivers such a line whole --
-// measured, not architected: profiles/r46_ll128_probe.jsonl (0 torn lines in 567 M racing
-// reads; the negative control tears 70-88%).  Line k holds payload pairs [15k, 15k+15).
-// The receiver zeroes every line it consumed: the small-message SGD kernel uses the same
-// slots in the LL format, whose flag test a stale LL128 payload word must never satisfy.
-// ---------------------------------------------------------------------------------
-__device__ __forceinline__ const uint4 *ll128_slot(const uint4 *slot) {
-    return reinterpret_cast<const uint4 *>((reinterpret_cast<uintptr_t>(slot) + 127) & ~uintptr_t(127));
-}
-
-template <typename TG, int WORLD>
-__global__ void __launch_bounds__(512, 2)   // 2 CTAs/SM: launch_gdraa_ll's resident grid
-gdraa_ll128_kernel(const __grid_constant__ KParams p) {
-    const int vr = blockIdx.y;
-    const int rank = p.rank0 + vr;
-    Pad *mine = p.pad[vr][rank];
-    __shared__ int s_last;
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint64_t epoch = *reinterpret_cast<volatile uint64_t *>(&mine->epoch) + 1;
-    const uint32_t flag = static_cast<uint32_t>(epoch);
-    const uint64_t par = epoch & 1u;
-    const uint64_t nbytes = p.n * sizeof(TG);
-    const uint64_t nlines = (nbytes + 119) / 120;
-    void *const buf = p.dst[vr][rank];
-    const int j = threadIdx.x & 7;
-    const unsigned gmask = 0xFFu << (threadIdx.x & 24);
-    const uint64_t groups = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 8);
-    bool ok = true;
-    // group-uniform loop: every lane of an 8-lane group handles the same line k
-    for (uint64_t k = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 8;
-         k < nlines; k += groups) {
-        const uint64_t pr = 15 * k + 2 * j;                 // first payload pair of this lane
-        const uint2 a = load_pair(buf, pr, nbytes);
-        const uint2 b = j < 7 ? load_pair(buf, pr + 1, nbytes) : make_uint2(flag, flag);
-        const uint4 entry = make_uint4(a.x, a.y, b.x, b.y);
-#pragma unroll
-        for (int kk = 1; kk < WORLD; ++kk) {   // push the line to every peer's slot [par][rank]
-            const int q = (rank + kk) % WORLD;
-            uint4 *dst = const_cast<uint4 *>(ll128_slot(p.ll[vr][q] + (par * WORLD + rank) * p.ll_pairs));
-            __syncwarp(gmask);   // the 8 lanes store the line in one instruction
-            st_ll(dst + k * 8 + j, entry);
-        }
-        uint32_t w[4][WORLD];
-#pragma unroll
-        for (int q = 0; q < WORLD; ++q) {
-            uint4 r = entry;
-            if (q != rank) {
-                const uint4 *src = ll128_slot(p.ll[vr][rank] + (par * WORLD + q) * p.ll_pairs) + k * 8 + j;
-                const uint64_t t0 = global_timer_ns();
-                uint32_t polls = 0, sleep_ns = 32;
-                while (true) {
-                    __syncwarp(gmask);   // ... and load it in one
-                    r = ld_ll(src);
-                    const bool here = __shfl_sync(gmask, r.z == flag && r.w == flag, 7, 8);
-                    if (here) break;
-                    bool late = false;
-                    if ((++polls & 1023u) == 0)
-                        late = global_timer_ns() - t0 > p.timeout_ns ||
-                               (p.abort != nullptr && *p.abort != 0);
-                    if (__shfl_sync(gmask, late, 0, 8)) {
-                        ok = false;
-                        break;
-                    }
-                    if (p.ll_sleep_ns != 0) {
-                        __nanosleep(sleep_ns);
-                        sleep_ns = sleep_ns * 2 > p.ll_sleep_ns ? p.ll_sleep_ns : sleep_ns * 2;
-                    }
-                }
-                if (!ok) {
-                    if (j == 0) report_timeout(p.err, 1, q, vr);
-                    break;
-                }
-                // consumed: clear the line, so that no stale payload word of it can ever
-                // pass for a flag of the LL-format kernels sharing this slot (the next
-                // writer of this parity comes after this call completes, as for LL)
-                st_ll(const_cast<uint4 *>(src), make_uint4(0u, 0u, 0u, 0u));
-            }
-            w[0][q] = r.x;
-            w[1][q] = r.y;
-            w[2][q] = r.z;
-            w[3][q] = r.w;
-        }
-        if (!ok) break;
-        store_pair(buf, pr, nbytes,
-                   make_uint2(WordMean<TG, WORLD>::run(w[0]), WordMean<TG, WORLD>::run(w[1])));
-        if (j < 7)
-            store_pair(buf, pr + 1, nbytes,
-                       make_uint2(WordMean<TG, WORLD>::run(w[2]), WordMean<TG, WORLD>::run(w[3])));
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __syncthreads();
@@ -1050,6 +943,9 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     if (warp == 0) {
         // producer: a3 loads (and the local w, v) of one chunk per stage
         if (lane == 0) {
+            // The entry barrier's acquire (generic proxy) must also order the bulk copies
+            // (async proxy) that read the peers' gradients after it.
+            asm volatile("fence.proxy.async.global;" ::: "memory");
             bool tail = false;
             for (uint32_t it = 0;; ++it) {
                 const int s = it % C::STAGES;
@@ -1177,9 +1073,11 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(2);
     GDRAA_STAMP_DONE();
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (WORLD > 1) fence_acq_rel_sys();
+    const bool cta_fence = (p.flags & kFlagCtaFence) != 0;
+    if (WORLD > 1 && !cta_fence) fence_acq_rel_sys();
     __syncthreads();
     if (threadIdx.x == 0) {
+        if (WORLD > 1 && cta_fence) fence_acq_rel_sys();
         const unsigned prev = atomicAdd(&mine->arrive, 1u);
         s_last = (prev == gridDim.x - 1);
         if (s_last) __threadfence();
@@ -1243,20 +1141,6 @@ KernelFnLL pick_ll_t(int world) {
         case 6: return gdraa_ll_kernel<TG, 6>;
         case 7: return gdraa_ll_kernel<TG, 7>;
         case 8: return gdraa_ll_kernel<TG, 8>;
-        default: return nullptr;
-    }
-}
-
-template <typename TG>
-KernelFnLL pick_ll128_t(int world) {
-    switch (world) {
-        case 2: return gdraa_ll128_kernel<TG, 2>;
-        case 3: return gdraa_ll128_kernel<TG, 3>;
-        case 4: return gdraa_ll128_kernel<TG, 4>;
-        case 5: return gdraa_ll128_kernel<TG, 5>;
-        case 6: return gdraa_ll128_kernel<TG, 6>;
-        case 7: return gdraa_ll128_kernel<TG, 7>;
-        case 8: return gdraa_ll128_kernel<TG, 8>;
         default: return nullptr;
     }
 }
@@ -1427,49 +1311,26 @@ cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows, boo
     return launch_pdl(l.fn, grid, block, s, p);
 }
 
-int ll128_mode() {
-    static const int v = [] {
-        // experimental, off unless asked for: GDRAA_LL128=1 (always) or =auto (by size).
-        // A virtual-rank SGD parity test failed once with the SGD form served by size
-        // (profiles/r51_pytest_gpu_n4.log) after passing twice; until that is understood
-        // neither LL128 kernel is on the default path.
-        const char *e = std::getenv("GDRAA_LL128");
-        if (e == nullptr || *e == 0) return 0;
-        return e[0] == '1' ? 1 : e[0] == 'a' ? 2 : 0;
-    }();
-    return v;
-}
-
-bool ll128_for(uint64_t nbytes, int world, uint64_t min_bytes) {
-    const int m = ll128_mode();
-    if (m != 2) return m == 1;
-    if (min_bytes != 0) return nbytes * static_cast<uint64_t>(world - 1) >= min_bytes;
-    // measured crossover (profiles/r48_sweep_n*_ll128_*.jsonl): the line format wins from
-    // ~512 KiB at N = 2 and ~256 KiB at N = 4, where LL's 2x bytes dominate; below, the
-    // LL entries' shorter poll path wins by <= 0.8 us
-    return nbytes * static_cast<uint64_t>(world - 1) >= kLL128MinBytes;
-}
-
 cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool cooperative,
                             cudaStream_t s) {
-    const bool l128 = ll128_for(p.n * (dtype == GDRAA_F32 ? 4 : 2), p.world);
-    KernelFnLL fn = l128 ? (dtype == GDRAA_F32 ? pick_ll128_t<float>(p.world)
-                                               : pick_ll128_t<__nv_bfloat16>(p.world))
-                         : (dtype == GDRAA_F32 ? pick_ll_t<float>(p.world)
-                                               : pick_ll_t<__nv_bfloat16>(p.world));
+    KernelFnLL fn = dtype == GDRAA_F32 ? pick_ll_t<float>(p.world)
+                                       : pick_ll_t<__nv_bfloat16>(p.world);
     if (fn == nullptr) return cudaErrorInvalidValue;
     const uint64_t es = dtype == GDRAA_F32 ? 4 : 2;
     if (p.n * es > 8 * p.ll_pairs) return cudaErrorInvalidValue;
-    // LL128: lines from the first 128-byte boundary of the slot must fit in it
-    if (l128 && 128 + (p.n * es + 119) / 120 * 128 > 16 * p.ll_pairs) return cudaErrorInvalidValue;
     constexpr int kT = 512;
-    // threads needed: one per 8-byte pair (LL) or 8 per 120-byte line (LL128)
-    const uint64_t npairs = l128 ? (p.n * es + 119) / 120 * 8 : (p.n * es + 7) / 8;
+    const uint64_t npairs = (p.n * es + 7) / 8;   // one thread per 8-byte payload pair
     int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
     uint64_t gx = (npairs + kT - 1) / kT;
-    const uint64_t cap = static_cast<uint64_t>(sms) * 2 / vr_rows;   // all resident
+    // all resident (2 CTAs of 512 per SM); GDRAA_MAX_CTAS caps it further, e.g. to leave
+    // SMs to a concurrent backward pass -- the grid-stride loop is correct at any size
+    uint64_t cap = static_cast<uint64_t>(sms) * 2 / vr_rows;
+    const int env_cap = env_max_ctas();
+    if (env_cap > 0 && static_cast<uint64_t>(env_cap) < cap) cap = env_cap;
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
     dim3 grid(static_cast<unsigned>(gx), vr_rows), block(kT);
@@ -1479,181 +1340,6 @@ cudaError_t launch_gdraa_ll(const KParams &p, int dtype, int vr_rows, bool coope
                                            0, s);
     }
     return launch_pdl(fn, grid, block, s, p);
-}
-
-namespace {
-// Poll one LL128 line (this lane's 16 bytes of it) until lane 7 of the 8-lane group sees
-// the flag; group-uniform result.  Bounded like ll_wait; on give-up ok = false.
-__device__ __forceinline__ uint4 ll128_wait(const uint4 *src, uint32_t flag, unsigned gmask,
-                                            const KParams &p, bool &ok) {
-    const uint64_t t0 = global_timer_ns();
-    uint32_t polls = 0, sleep_ns = 32;
-    while (true) {
-        __syncwarp(gmask);   // the 8 lanes load the line in one instruction
-        const uint4 r = ld_ll(src);
-        if (__shfl_sync(gmask, r.z == flag && r.w == flag, 7, 8)) return r;
-        bool late = false;
-        if ((++polls & 1023u) == 0)
-            late = global_timer_ns() - t0 > p.timeout_ns || (p.abort != nullptr && *p.abort != 0);
-        if (__shfl_sync(gmask, late, 0, 8)) {
-            ok = false;
-            return r;
-        }
-        if (p.ll_sleep_ns != 0) {
-            __nanosleep(sleep_ns);
-            sleep_ns = sleep_ns * 2 > p.ll_sleep_ns ? p.ll_sleep_ns : sleep_ns * 2;
-        }
-    }
-}
-}  // namespace
-
-// LL128 form of the small-message SGD step for fp32 gradients and fp32 w (kSgd): the same
-// three phases, slot parity rule, fold and update as gdraa_ll_sgd_kernel, with every
-// transfer in 128-byte lines of 120 payload bytes (30 elements) + flag, as the LL128 mean.
-// Lane j of an 8-lane group owns elements [30k + 4j, +4) of line k (lane 7: 2 elements +
-// the flag); the gradient line k and the broadcast line k of a block cover the same
-// elements (4-byte g and w').  Slot of a sender: lines [0, RL) gradient block, [RL, 2RL)
-// updated block, RL = ceil(4 blk / 120).  Consumed lines are cleared (LL kernels share
-// the slots).
-template <int WORLD>
-__global__ void __launch_bounds__(512, 2)
-gdraa_ll128_sgd_kernel(const __grid_constant__ KParams p) {
-    const int vr = blockIdx.y;
-    const int rank = p.rank0 + vr;
-    Pad *mine = p.pad[vr][rank];
-    __shared__ int s_last;
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint64_t epoch = *reinterpret_cast<volatile uint64_t *>(&mine->epoch) + 1;
-    const uint32_t flag = static_cast<uint32_t>(epoch);
-    const uint64_t par = epoch & 1u;
-    const uint64_t RL = (p.blk * 4 + 119) / 120;
-    const int j = threadIdx.x & 7;
-    const unsigned gmask = 0xFFu << (threadIdx.x & 24);
-    const uint64_t g0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 8;
-    const uint64_t groups = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 8);
-    auto shard = [&](int q, uint64_t &o, uint64_t &l) {
-        o = min(static_cast<uint64_t>(q) * p.blk, p.n);
-        l = min(p.blk, p.n - o);
-    };
-    auto rx = [&](int q) {
-        return const_cast<uint4 *>(ll128_slot(p.ll[vr][rank] + (par * WORLD + q) * p.ll_pairs));
-    };
-    auto tx = [&](int q) {
-        return const_cast<uint4 *>(ll128_slot(p.ll[vr][q] + (par * WORLD + rank) * p.ll_pairs));
-    };
-    const float *const gl = static_cast<const float *>(p.src[vr][rank]);
-    bool ok = true;
-
-    // A: push block D(rank, q) to every owner q != rank.
-    #pragma unroll 1
-    for (int k = 1; k < WORLD; ++k) {
-        const int q = (rank + k) % WORLD;
-        uint64_t oq, lq;
-        shard(q, oq, lq);
-        const uint64_t nb = lq * 4, nl = (nb + 119) / 120;
-        const float *base = gl + oq;
-        uint4 *dst = tx(q);
-        for (uint64_t ln = g0; ln < nl; ln += groups) {
-            const uint64_t pr = 15 * ln + 2 * j;
-            const uint2 a = load_pair(base, pr, nb);
-            const uint2 b = j < 7 ? load_pair(base, pr + 1, nb) : make_uint2(flag, flag);
-            __syncwarp(gmask);
-            st_ll(dst + ln * 8 + j, make_uint4(a.x, a.y, b.x, b.y));
-        }
-    }
-
-    // B: fold + update our block line by line, push w' lines to every peer.
-    uint64_t off, len;
-    shard(rank, off, len);
-    float *const vloc = p.v[vr];
-    float *const wloc = static_cast<float *>(p.dst[vr][rank]);
-    const float lr = p.lr, mom = p.mom, wd = p.wd;
-    const uint64_t nl_own = (len * 4 + 119) / 120;
-    for (uint64_t ln = g0; ok && ln < nl_own; ln += groups) {
-        const uint64_t i0 = 30 * ln + 4 * j;                       // shard-relative
-        const int cap_e = j < 7 ? 4 : 2;
-        const int cnt = i0 >= len ? 0 : static_cast<int>(len - i0 < static_cast<uint64_t>(cap_e)
-                                                             ? len - i0 : cap_e);
-        float x[WORLD][4];
-#pragma unroll
-        for (int q = 0; q < WORLD; ++q) {
-            if (q == rank) {
-                for (int e = 0; e < 4; ++e) x[q][e] = e < cnt ? gl[off + i0 + e] : 0.f;
-                continue;
-            }
-            uint4 *src = rx(q) + ln * 8 + j;
-            const uint4 r = ll128_wait(src, flag, gmask, p, ok);
-            if (!ok) {
-                if (j == 0) report_timeout(p.err, 1, q, vr);
-                break;
-            }
-            st_ll(src, make_uint4(0u, 0u, 0u, 0u));
-            x[q][0] = __uint_as_float(r.x);
-            x[q][1] = __uint_as_float(r.y);
-            x[q][2] = __uint_as_float(r.z);
-            x[q][3] = __uint_as_float(r.w);
-        }
-        if (!ok) break;
-        uint32_t ow[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if (e >= cnt) break;
-            float col[WORLD];
-#pragma unroll
-            for (int q = 0; q < WORLD; ++q) col[q] = x[q][e];
-            const float m = average<WORLD>(col);
-            float wv = wloc[off + i0 + e], vv = vloc[off + i0 + e];
-            sgd(m, lr, mom, wd, wv, vv);
-            vloc[off + i0 + e] = vv;
-            wloc[off + i0 + e] = wv;
-            ow[e] = __float_as_uint(wv);
-        }
-        const uint4 line = j < 7 ? make_uint4(ow[0], ow[1], ow[2], ow[3])
-                                 : make_uint4(ow[0], ow[1], flag, flag);
-#pragma unroll
-        for (int k = 1; k < WORLD; ++k) {
-            __syncwarp(gmask);   // the 8 lanes store the line in one instruction
-            st_ll(tx((rank + k) % WORLD) + (RL + ln) * 8 + j, line);
-        }
-    }
-
-    // C: receive every peer's updated block into our w.
-#pragma unroll 1
-    for (int k = 1; ok && k < WORLD; ++k) {
-        const int q = (rank + k) % WORLD;
-        uint64_t oq, lq;
-        shard(q, oq, lq);
-        const uint64_t nb = lq * 4, nl = (nb + 119) / 120;
-        float *base = wloc + oq;
-        for (uint64_t ln = g0; ln < nl; ln += groups) {
-            uint4 *src = rx(q) + (RL + ln) * 8 + j;
-            const uint4 r = ll128_wait(src, flag, gmask, p, ok);
-            if (!ok) {
-                if (j == 0) report_timeout(p.err, 2, q, vr);
-                break;
-            }
-            st_ll(src, make_uint4(0u, 0u, 0u, 0u));
-            const uint64_t pr = 15 * ln + 2 * j;
-            store_pair(base, pr, nb, make_uint2(r.x, r.y));
-            if (j < 7) store_pair(base, pr + 1, nb, make_uint2(r.z, r.w));
-        }
-    }
-
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned prev = atomicAdd(&mine->arrive, 1u);
-        s_last = (prev == gridDim.x - 1);
-        if (s_last) __threadfence();
-    }
-    __syncthreads();
-    if (s_last && threadIdx.x == 0) {
-        mine->arrive = 0;
-        mine->calls += 1;
-        mine->ll_calls += 1;
-        mine->epoch = epoch;
-        if (p.done[vr] != nullptr) *p.done[vr] = epoch;
-    }
 }
 
 namespace {
@@ -1677,35 +1363,10 @@ bool ll_sgd_fits(uint64_t blk, int dtype, int mode, uint64_t ll_pairs) {
     return (blk * sg + 7) / 8 + (blk * sw + 7) / 8 <= ll_pairs;
 }
 
-namespace {
-KernelFnLL pick_ll128_sgd(int world) {
-    switch (world) {
-        case 2: return gdraa_ll128_sgd_kernel<2>;
-        case 3: return gdraa_ll128_sgd_kernel<3>;
-        case 4: return gdraa_ll128_sgd_kernel<4>;
-        case 5: return gdraa_ll128_sgd_kernel<5>;
-        case 6: return gdraa_ll128_sgd_kernel<6>;
-        case 7: return gdraa_ll128_sgd_kernel<7>;
-        case 8: return gdraa_ll128_sgd_kernel<8>;
-        default: return nullptr;
-    }
-}
-}  // namespace
-
 cudaError_t launch_gdraa_ll_sgd(const KParams &p, int dtype, int mode, int vr_rows,
                                 bool cooperative, cudaStream_t s) {
     KernelFnLL fn = nullptr;
-    // LL128 lines for fp32 gradients + fp32 w from n * 4 * (N-1) >= 3 MiB (measured at
-    // N = 2, profiles/r50_sweep_sgd_n2_ll128_*.jsonl: 1.18x at 4 MiB = config 1, 0.92-0.95x
-    // from 1 KiB to 2 MiB), when the two line regions fit the slot past its first
-    // 128-byte boundary
-    const uint64_t rl = (p.blk * 4 + 119) / 120;
-    const bool l128 = dtype == GDRAA_F32 && mode == kSgd &&
-                      ll128_for(p.n * 4, p.world, kLL128SgdMinBytes) &&
-                      128 + 2 * rl * 128 <= 16 * p.ll_pairs;
-    if (l128)
-        fn = pick_ll128_sgd(p.world);
-    else if (mode == kSgd)
+    if (mode == kSgd)
         fn = dtype == GDRAA_F32 ? pick_ll_sgd_m<float, kSgd>(p.world)
                                 : pick_ll_sgd_m<__nv_bfloat16, kSgd>(p.world);
     else if (mode == kSgdMp)
@@ -1723,11 +1384,14 @@ cudaError_t launch_gdraa_ll_sgd(const KParams &p, int dtype, int mode, int vr_ro
     if (e != cudaSuccess) return e;
     // every CTA polls entries other CTAs (and peers) produce: the grid must be resident
     const uint64_t es = dtype == GDRAA_F32 ? 4 : 2;
-    const uint64_t work = l128 ? rl * 8
-                               : ((p.blk * es + 7) / 8 > (p.blk + E - 1) / E ? (p.blk * es + 7) / 8
-                                                                             : (p.blk + E - 1) / E);
+    const uint64_t rs_pairs = (p.blk * es + 7) / 8, units = (p.blk + E - 1) / E;
+    const uint64_t work = rs_pairs > units ? rs_pairs : units;
     uint64_t gx = (work + kT - 1) / kT;
-    const uint64_t cap = static_cast<uint64_t>(sms) * per_sm / vr_rows;
+    // GDRAA_MAX_CTAS caps it further (a smaller grid is resident all the more; every
+    // phase is a grid-stride loop)
+    uint64_t cap = static_cast<uint64_t>(sms) * per_sm / vr_rows;
+    const int env_cap = env_max_ctas();
+    if (env_cap > 0 && static_cast<uint64_t>(env_cap) < cap) cap = env_cap;
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
     dim3 grid(static_cast<unsigned>(gx), vr_rows), block(kT);

@@ -148,6 +148,15 @@ struct State {
     uint64_t timeout_ns = 30000000000ull;
     bool gated = false;
     uint64_t issued = 0;
+    // Cross-stream ordering: every call shares this rank's pad (epoch, arrival and work
+    // counters) and LL slots, so a call issued on another stream than the previous one
+    // first waits for everything issued so far on the previous call's stream (an event
+    // recorded there at that moment; calls on one stream pay nothing, and programmatic
+    // dependent launch between them is kept).  Not while either stream is capturing:
+    // a graph's own edges order the calls captured into it.
+    cudaStream_t last_stream = nullptr;
+    cudaEvent_t order_ev = nullptr;
+    bool have_last = false;
     bool fatal = false;
     int fatal_code = 0;
     std::string fatal_msg;
@@ -337,6 +346,7 @@ void fill_common(KParams &p, uint64_t n) {
     }
     p.ll_pairs = g.ll_pairs;
     p.ll_sleep_ns = static_cast<uint32_t>(env_u64("GDRAA_LL_SLEEP_NS", 256));
+    p.flags = env_kernel_flags();
     p.err = g.err_d;
     p.done[0] = g.done_d;
     p.abort = g.abort_d;
@@ -354,6 +364,29 @@ void account(uint64_t n, int dtype_g, uint64_t s_w) {
     g.host.adds += n1 * len;
     g.host.divides += len;
     g.host.launches += 1;
+}
+
+bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone;
+}
+
+// Before a launch on s: order it after the previous call if that was on another stream.
+int order_after_previous(cudaStream_t s) {
+    if (!g.have_last || s == g.last_stream || capturing(s) || capturing(g.last_stream))
+        return GDRAA_OK;
+    if (g.order_ev == nullptr)
+        CUDA_TRY(cudaEventCreateWithFlags(&g.order_ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(g.order_ev, g.last_stream));
+    CUDA_TRY(cudaStreamWaitEvent(s, g.order_ev, 0));
+    return GDRAA_OK;
+}
+
+// After a launch on s: remember the stream.
+int note_launch(cudaStream_t s) {
+    g.last_stream = s;
+    g.have_last = true;
+    return GDRAA_OK;
 }
 
 int launch(const KParams &p, int dtype, int mode, cudaStream_t s) {
@@ -377,6 +410,14 @@ struct VrDevice {
 };
 
 }  // namespace
+
+uint32_t env_kernel_flags() {
+    static const uint32_t v = [] {
+        const char *e = std::getenv("GDRAA_EXIT_FENCE");
+        return (e != nullptr && std::strcmp(e, "cta") == 0) ? kFlagCtaFence : 0u;
+    }();
+    return v;
+}
 
 uint64_t ll_limit_bytes(int world) {
     if (world < 2) return 0;
@@ -500,6 +541,7 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
     p.err = d->err_d;
     p.ll_pairs = d->ll[world] != nullptr ? d->ll_pairs[world] : 0;
     p.ll_sleep_ns = static_cast<uint32_t>(env_u64("GDRAA_LL_SLEEP_NS", 256));
+    p.flags = env_kernel_flags();
     const size_t es = dtype == GDRAA_F32 ? 4 : 2;
     if (mode == kMean && world > 1 && n * es <= 8 * p.ll_pairs) {   // latency path
         cudaError_t e = launch_gdraa_ll(p, dtype, world, true, s);
@@ -575,6 +617,7 @@ static void release_resources() {
     if (g.page_registered) cudaHostUnregister(g.page);
     if (g.page) munmap(g.page, 4096);
     if (g.err_h) cudaFreeHost(g.err_h);
+    if (g.order_ev) cudaEventDestroy(g.order_ev);
     State s;
     g = s;
 }
@@ -700,13 +743,13 @@ static int init_impl(int world, int rank) {
     if (world > 1) {
         proto::Reg cfg{};
         cfg.what = 3;
-        cfg.n = g.ll_sgd_limit | (static_cast<uint64_t>(ll128_mode()) << 62);   // + LL format rule
+        cfg.n = g.ll_sgd_limit;
         cfg.dtype = static_cast<int32_t>(std::min<uint64_t>(g.ll_pairs, INT32_MAX));
         proto::RegOk all{};
         int rc = exchange(cfg, &all);
         if (rc == GDRAA_ESHAPE)
             rc = fail(GDRAA_ESHAPE, "ranks disagree on the small-message thresholds "
-                      "(GDRAA_LL_MAX_BYTES / GDRAA_LL_SGD_MAX_BYTES / GDRAA_LL128 must match on every "
+                      "(GDRAA_LL_MAX_BYTES / GDRAA_LL_SGD_MAX_BYTES must match on every "
                       "rank): %s",
                       t_err.c_str());
         if (rc) return cleanup_fail(rc);
@@ -790,17 +833,20 @@ static int mean_common(void *buf, size_t first, size_t count, gdraa_stream_t s) 
         p.src[0][q] = offset_ptr(r->peer[q], first, es);
         p.dst[0][q] = offset_ptr(r->peer[q], first, es);
     }
+    const cudaStream_t cs = reinterpret_cast<cudaStream_t>(s);
+    rc = order_after_previous(cs);
+    if (rc) return rc;
     if (g.ll != nullptr && count * es <= 8 * g.ll_pairs) {
         // small message: the latency path (same result, bit for bit)
-        cudaError_t e = launch_gdraa_ll(p, r->dtype, 1, false, reinterpret_cast<cudaStream_t>(s));
+        cudaError_t e = launch_gdraa_ll(p, r->dtype, 1, false, cs);
         if (e != cudaSuccess) return fail(GDRAA_ECUDA, "LL kernel launch: %s", cudaGetErrorString(e));
         g.issued += 1;
     } else {
-        rc = launch(p, r->dtype, kMean, reinterpret_cast<cudaStream_t>(s));
+        rc = launch(p, r->dtype, kMean, cs);
         if (rc) return rc;
     }
     account(count, r->dtype, 0);
-    return GDRAA_OK;
+    return note_launch(cs);
 }
 
 int gdraa_allreduce_mean(void *buf, gdraa_stream_t s) { return mean_common(buf, 0, SIZE_MAX, s); }
@@ -851,19 +897,21 @@ static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, 
     }
     p.v[0] = static_cast<float *>(offset_ptr(v, first, 4));
     p.wm[0] = mode == kSgdMp ? static_cast<float *>(offset_ptr(wm, first, 4)) : nullptr;
+    const cudaStream_t cs = reinterpret_cast<cudaStream_t>(s);
+    rc = order_after_previous(cs);
+    if (rc) return rc;
     if (g.ll != nullptr && count * eg <= g.ll_sgd_limit &&
         ll_sgd_fits(p.blk, rg->dtype, mode, g.ll_pairs)) {
         // small message: the data carries both synchronisations (same result, bit for bit)
-        cudaError_t e = launch_gdraa_ll_sgd(p, rg->dtype, mode, 1, false,
-                                            reinterpret_cast<cudaStream_t>(s));
+        cudaError_t e = launch_gdraa_ll_sgd(p, rg->dtype, mode, 1, false, cs);
         if (e != cudaSuccess) return fail(GDRAA_ECUDA, "LL SGD kernel launch: %s", cudaGetErrorString(e));
         g.issued += 1;
     } else {
-        rc = launch(p, rg->dtype, mode, reinterpret_cast<cudaStream_t>(s));
+        rc = launch(p, rg->dtype, mode, cs);
         if (rc) return rc;
     }
     account(count, rg->dtype, mode == kSgd ? 4 : 2);
-    return GDRAA_OK;
+    return note_launch(cs);
 }
 
 int gdraa_sgd_step(float *w, const void *gr, float *v, float lr, float mom, gdraa_stream_t s) {
@@ -911,6 +959,8 @@ int gdraa_get_stats(gdraa_stats_t *out) {
     out->calls = host.calls;
     out->sync_waits = host.sync_waits;
     out->ll_calls = host.ll_calls;
+    out->iter_done = g.page ? g.page->done[g.rank] : 0;
+    out->iter_start = g.page ? g.page->go[g.rank] : 0;
     return GDRAA_OK;
 }
 
@@ -964,6 +1014,62 @@ int gdraa_vr_sgd_step_mp(int world, float *const *w_master, void *const *w_model
     std::lock_guard<std::mutex> lk(g_mu);
     VrArgs a{world, g_, w_model, v, w_master, n, dtype, lr, mom, wd, kSgdMp};
     return vr_run(a, reinterpret_cast<cudaStream_t>(s));
+}
+
+// Bucketed virtual-rank calls: the same kernels on [first, first + count) of every rank's
+// buffers (the owner rule of gdraa_sgd_step_range applies to the range).
+static int vr_range(VrArgs a, size_t first, size_t count, cudaStream_t s) {
+    if (a.world < 1 || a.world > kMaxWorld) return fail(GDRAA_EINVAL, "world %d out of [1,%d]", a.world, kMaxWorld);
+    if (count == 0) return fail(GDRAA_EINVAL, "count must be >= 1");
+    if (first % 8 != 0) return fail(GDRAA_EINVAL, "first (%zu) must be a multiple of 8", first);
+    if (first > a.n || count > a.n - first)
+        return fail(GDRAA_EINVAL, "range [%zu, %zu) exceeds the %zu elements", first,
+                    first + count, a.n);
+    if (a.src == nullptr || a.dst == nullptr || (a.mode != kMean && a.v == nullptr) ||
+        (a.mode == kSgdMp && a.wm == nullptr))
+        return fail(GDRAA_EINVAL, "null pointer array");
+    const size_t eg = a.dtype == GDRAA_F32 ? 4 : 2;
+    const size_t ed = a.mode == kSgd ? 4 : (a.mode == kSgdMp ? 2 : eg);
+    const void *src[kMaxWorld];
+    void *dst[kMaxWorld];
+    float *v[kMaxWorld], *wm[kMaxWorld];
+    for (int q = 0; q < a.world; ++q) {
+        src[q] = offset_ptr(const_cast<void *>(a.src[q]), first, eg);
+        dst[q] = offset_ptr(a.dst[q], first, ed);
+        v[q] = a.v ? static_cast<float *>(offset_ptr(a.v[q], first, 4)) : nullptr;
+        wm[q] = a.wm ? static_cast<float *>(offset_ptr(a.wm[q], first, 4)) : nullptr;
+    }
+    a.src = src;
+    a.dst = dst;
+    a.v = a.v ? v : nullptr;
+    a.wm = a.wm ? wm : nullptr;
+    a.n = count;
+    return vr_run(a, s);
+}
+
+int gdraa_vr_allreduce_mean_range(int world, void *const *bufs, size_t n, int dtype,
+                                  size_t first, size_t count, gdraa_stream_t s) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    VrArgs a{world, reinterpret_cast<const void *const *>(bufs), bufs, nullptr, nullptr, n, dtype,
+             0.f, 0.f, 0.f, kMean};
+    return vr_range(a, first, count, reinterpret_cast<cudaStream_t>(s));
+}
+
+int gdraa_vr_sgd_step_range(int world, float *const *w, const void *const *g_, float *const *v,
+                            size_t n, int dtype, size_t first, size_t count, float lr, float mom,
+                            float wd, gdraa_stream_t s) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    VrArgs a{world, g_, reinterpret_cast<void *const *>(w), v, nullptr, n, dtype, lr, mom, wd, kSgd};
+    return vr_range(a, first, count, reinterpret_cast<cudaStream_t>(s));
+}
+
+int gdraa_vr_sgd_step_mp_range(int world, float *const *w_master, void *const *w_model,
+                               const void *const *g_, float *const *v, size_t n, int dtype,
+                               size_t first, size_t count, float lr, float mom, float wd,
+                               gdraa_stream_t s) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    VrArgs a{world, g_, w_model, v, w_master, n, dtype, lr, mom, wd, kSgdMp};
+    return vr_range(a, first, count, reinterpret_cast<cudaStream_t>(s));
 }
 
 }  // extern "C"

@@ -6,8 +6,10 @@
 // HELLO, relays CUDA IPC handles for every registration after checking that n / dtype
 // agree (S:177 shape-mismatch), owns the shared go/done page the kernels write their
 // per-iteration completion into, and ends with a collective BYE.  It never opens an IPC
-// handle and links no CUDA library, so it cannot touch weight data: the page's
-// data_bytes counter is 0 by construction and is reported at exit.
+// handle and links no CUDA library, so it cannot touch weight data (structural evidence:
+// tests/test_jobserver.py::test_jobserver_links_no_cuda).  Its data_bytes counter counts
+// the payload of any message outside the control vocabulary (the sender is dropped) and
+// is reported at exit.
 #include <fcntl.h>
 #include <poll.h>
 #include <sys/mman.h>
@@ -107,6 +109,9 @@ struct Server {
         if (c.gone) return;
         c.gone = true;
         ::close(c.fd);
+        // A connection that never completed HELLO is not a rank of this job (a readiness
+        // probe, a stale rank of an earlier job): close it without failing the job.
+        if (!c.hello) return;
         if (!c.bye && !failed) {   // the first failure is the one reported
             failed = true;
             fail_msg = "rank " + std::to_string(c.rank) + " disconnected (" + why + ")";
@@ -194,6 +199,12 @@ struct Server {
                 return;
             }
             default:
+                // Not a control message.  None of the protocol's kinds carries tensor
+                // data, so the payload of anything else is counted as data and its sender
+                // dropped: data_bytes is a guard that reads 0 only if no rank ever tried
+                // to move data through the job server.
+                page->data_bytes = page->data_bytes + body.size();
+                page->control_bytes = page->control_bytes - sizeof h - body.size();
                 return drop(c, "unknown message");
         }
     }

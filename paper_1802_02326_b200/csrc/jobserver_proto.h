@@ -8,7 +8,8 @@
 //   BYE / BYE_OK       collective shutdown                                  (S:95 Shutdown)
 // and a POSIX shared-memory page with per-rank go/done counters (S:95 IterStart /
 // IterDone) that the kernels' last CTA writes through a host mapping.  No message type
-// carries tensor data; `data_bytes` in the page counts any that would and stays 0.
+// carries tensor data; `data_bytes` in the page counts the payload of any message outside
+// this vocabulary (its sender is dropped), so it reads 0 unless something tried.
 // Plain C structs; both sides are the same binary architecture (one node).
 #pragma once
 
@@ -84,7 +85,7 @@ struct alignas(64) ShmPage {
     volatile int32_t abort;                 // set by the job server if a rank vanished
     volatile int32_t dead_rank;
     volatile uint64_t control_bytes;        // bytes of control messages handled
-    volatile uint64_t data_bytes;           // bytes of weight/gradient data handled: 0
+    volatile uint64_t data_bytes;           // payload bytes of non-control messages (dropped)
     volatile uint64_t registrations;
 };
 

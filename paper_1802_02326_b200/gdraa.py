@@ -25,7 +25,9 @@ EXPORTED = ["gdraa_sgd_step_ex", "gdraa_sgd_step_mp", "gdraa_poly_lr",
             "gdraa_vr_sgd_step_ex", "gdraa_vr_sgd_step_mp",
             "gdraa_init", "gdraa_register", "gdraa_deregister","gdraa_allreduce_mean", "gdraa_sgd_step",
             "gdraa_shard", "gdraa_get_stats", "gdraa_finalize", "gdraa_last_error",
-            "gdraa_version", "gdraa_vr_allreduce_mean", "gdraa_vr_sgd_step"]
+            "gdraa_version", "gdraa_vr_allreduce_mean", "gdraa_vr_sgd_step",
+            "gdraa_vr_allreduce_mean_range", "gdraa_vr_sgd_step_range",
+            "gdraa_vr_sgd_step_mp_range"]
 
 
 class GdraaError(RuntimeError):
@@ -38,7 +40,8 @@ class GdraaError(RuntimeError):
 class gdraa_stats_t(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in
                 ("calls", "sync_waits", "rs_bytes_in", "rs_bytes_out", "ag_bytes_out",
-                 "ag_bytes_in", "adds", "divides", "launches", "ll_calls")]
+                 "ag_bytes_in", "adds", "divides", "launches", "ll_calls", "iter_done",
+                 "iter_start")]
 
 
 if not os.path.exists(LIB_PATH):
@@ -74,6 +77,12 @@ _sig = {
                               ctypes.POINTER(_vp), _sz, _i, _f, _f, _f, _vp], _i),
     "gdraa_vr_sgd_step_mp": ([_i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                               ctypes.POINTER(_vp), _sz, _i, _f, _f, _f, _vp], _i),
+    "gdraa_vr_allreduce_mean_range": ([_i, ctypes.POINTER(_vp), _sz, _i, _sz, _sz, _vp], _i),
+    "gdraa_vr_sgd_step_range": ([_i, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                 ctypes.POINTER(_vp), _sz, _i, _sz, _sz, _f, _f, _f, _vp], _i),
+    "gdraa_vr_sgd_step_mp_range": ([_i, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                    ctypes.POINTER(_vp), ctypes.POINTER(_vp), _sz, _i, _sz, _sz,
+                                    _f, _f, _f, _vp], _i),
 }
 for _name, (_args, _res) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -252,3 +261,32 @@ def gdraa_vr_sgd_step_mp(w_master, w_model, g, v, lr: float, mom: float, wd: flo
     _check(_lib.gdraa_vr_sgd_step_mp(len(g), _ptr_array(w_master), _ptr_array(w_model),
                                      _ptr_array(g), _ptr_array(v), n, dtype_code(g[0]), lr, mom,
                                      wd, _stream(stream)), "gdraa_vr_sgd_step_mp")
+
+
+def gdraa_vr_allreduce_mean_range(bufs, first: int, count: int, stream=None):
+    """Bucketed form: [first, first + count) of every virtual rank's buffer."""
+    n = bufs[0].numel()
+    _same_numel(n, bufs)
+    _check(_lib.gdraa_vr_allreduce_mean_range(len(bufs), _ptr_array(bufs), n,
+                                              dtype_code(bufs[0]), first, count,
+                                              _stream(stream)),
+           "gdraa_vr_allreduce_mean_range")
+
+
+def gdraa_vr_sgd_step_range(w, g, v, first: int, count: int, lr: float, mom: float,
+                            wd: float = 0.0, stream=None):
+    n = g[0].numel()
+    _same_numel(n, w, g, v)
+    _check(_lib.gdraa_vr_sgd_step_range(len(g), _ptr_array(w), _ptr_array(g), _ptr_array(v), n,
+                                        dtype_code(g[0]), first, count, lr, mom, wd,
+                                        _stream(stream)), "gdraa_vr_sgd_step_range")
+
+
+def gdraa_vr_sgd_step_mp_range(w_master, w_model, g, v, first: int, count: int, lr: float,
+                               mom: float, wd: float = 0.0, stream=None):
+    n = g[0].numel()
+    _same_numel(n, w_master, w_model, g, v)
+    _check(_lib.gdraa_vr_sgd_step_mp_range(len(g), _ptr_array(w_master), _ptr_array(w_model),
+                                           _ptr_array(g), _ptr_array(v), n, dtype_code(g[0]),
+                                           first, count, lr, mom, wd, _stream(stream)),
+           "gdraa_vr_sgd_step_mp_range")

@@ -38,6 +38,17 @@ def test_reference_arm_line():
                         "d2h_bytes_per_step": 0}
 
 
+def test_self_launch_without_torchrun():
+    """`python bench.py --gpus N` with no WORLD_SIZE in the environment starts its own N
+    ranks (torch.distributed.run on a free 127.0.0.1 port); exactly one JSON line comes
+    back, from rank 0, with every rank present."""
+    d = _run(["--gpus", "2", "--steps", "3", "--warmup", "3", "--dry-launch"], 300)
+    assert d["dry_launch"] and d["world"] == 2 and d["n_gpus"] == 2
+    assert sorted(r["rank"] for r in d["ranks"]) == [0, 1]
+    assert sorted(r["local_rank"] for r in d["ranks"]) == [0, 1]
+    assert all(r["master_addr"] == "127.0.0.1" for r in d["ranks"])
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["graph", "eager"])
 def test_our_arm_line(mode):
@@ -51,9 +62,25 @@ def test_our_arm_line(mode):
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
     assert r["achieved"] == pytest.approx(r["bytes_per_launch"] / (d["ms_per_step"] * 1e-3) / 1e9)
-    assert d["value"] == pytest.approx(r["achieved"])     # N = 1: whole job = one rank
+    assert d["value"] == pytest.approx(r["achieved"])     # per-rank rate of the launch
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     pc = d["per_call"]
     assert pc["p10_us"] <= pc["median_us"] <= pc["p90_us"]
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+
+
+@pytest.mark.gpu
+@pytest.mark.multigpu
+@pytest.mark.skipif(not __import__("tests.conftest", fromlist=["x"]).has_cuda()
+                    or __import__("torch").cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_our_arm_self_launched_n2():
+    """The driver's form `python bench.py --gpus 2` (no torchrun): NVLink roofline line."""
+    d = _run(["--gpus", "2", "--steps", "20", "--warmup", "5", "--e2e-steps", "3"], 900)
+    assert d["n_gpus"] == 2 and d["config"]["path"] == "two_shot"
+    r = d["roofline"]
+    assert r["bound"] == "nvlink" and r["peak"] == 770.0 and 0 < r["frac"] < 1.2
+    assert "frac_of_nominal_900" in r
+    assert d["value"] == pytest.approx(r["achieved"]) == pytest.approx(d["bus_gbs_per_rank"])
+    assert d["job_total_gbs"] == pytest.approx(2 * d["value"])
+    assert d["nccl_reference"]["bus_gbs_per_rank"] > 0

@@ -23,14 +23,3 @@ def test_forced_kernel_parity(kernel):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert f"OK {kernel}" in r.stdout
 
-
-@pytest.mark.skipif(os.environ.get("GDRAA_TEST_LL128") != "1",
-                    reason="experimental LL128 kernels (off by default): GDRAA_TEST_LL128=1")
-def test_ll128_mean_parity():
-    """The experimental LL128 line format of the small-message mean and SGD step gives
-    the oracle's bits (not on the default path)."""
-    env = dict(os.environ, GDRAA_LL128="1")
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_ll128_worker.py")],
-                       env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert "OK ll128" in r.stdout

@@ -326,6 +326,22 @@ def test_world1_bucketed_ranges(world1):
         assert e.value.name == "GDRAA_EINVAL", bad
 
 
+def test_world1_iter_done_flag(world1):
+    """a0 at world 1: the kernel's last CTA writes IterDone into the go/done page
+    after every call, through both the two-shot/local and the mean kernels."""
+    L = 70_001
+    g = to_dev(synth.grad_like(14, 0, L))
+    w, v = to_dev(synth.w_like(14, L)), torch.zeros(L, device=DEV)
+    gdraa.gdraa_register(w)
+    gdraa.gdraa_register(g)
+    for k in range(1, 6):
+        gdraa.gdraa_sgd_step(w, g, v, 0.1, 0.9)
+        if k % 2 == 0:
+            gdraa.gdraa_allreduce_mean(g)
+        st = gdraa.gdraa_get_stats()
+        assert st["iter_done"] == st["calls"] == k + k // 2, st
+
+
 def test_world1_errors(world1):
     a = torch.zeros(1000, device=DEV)
     b = torch.zeros(1000, device=DEV)
@@ -428,3 +444,83 @@ def test_vr_sgd_step_mp(N, dt):
             keep = np.ones(L, bool)
             keep[off:off + ln] = False
             assert np.array_equal(wm[keep].view(np.uint32), w0[keep].view(np.uint32))
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT-3 across virtual ranks: buckets in backward (out-of-order) order, each with its own
+# owner partition, equal the whole-buffer oracle step.
+# ---------------------------------------------------------------------------------------
+
+def _buckets(L):
+    """Out-of-order buckets covering [0, L): starts multiples of 8, ragged sizes, one
+    bucket smaller than the world (empty shards), one above the small-message limit."""
+    cuts = sorted({0, 8, 64, 4104, L // 3 // 8 * 8, (L // 2 + 5) // 8 * 8, L})
+    spans = [(a, b - a) for a, b in zip(cuts, cuts[1:]) if b > a]
+    return spans[::-1]
+
+
+@pytest.mark.parametrize("N", [2, 3, 4, 8])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_vr_bucketed_ranges(N, dt):
+    bf16 = dt == "bf16"
+    L = 5_000_017
+    buckets = _buckets(L)
+    lim = gdraa.gdraa_small_step_bytes(N, gdraa.GDRAA_BF16 if bf16 else gdraa.GDRAA_F32)
+    sizes = [c * (2 if bf16 else 4) for _, c in buckets]
+    assert min(sizes) <= lim < max(sizes)           # both the LL and the two-shot kernel
+    gs = make_grads("like", 700 + N, N, L, bf16)
+    w0, v0 = synth.w_like(700 + N, L), synth.w_like(800 + N, L)
+    wd = 0.001
+    w_exp, v_exp = oracle.sgd_step_wd(gs, w0, v0, synth.PAPER_LR, synth.PAPER_MOM, wd)
+    g_d = [to_dev(g, bf16) for g in gs]
+    w_d = [to_dev(w0) for _ in range(N)]
+    v_d = [to_dev(v0) for _ in range(N)]
+    for first, count in buckets:
+        gdraa.gdraa_vr_sgd_step_range(w_d, g_d, v_d, first, count, synth.PAPER_LR,
+                                      synth.PAPER_MOM, wd)
+    torch.cuda.synchronize()
+    for r in range(N):
+        compare(from_dev(w_d[r]), w_exp, "f32", what=f"bucketed w N={N} r{r}")
+        vh, vmask = from_dev(v_d[r]), np.zeros(L, bool)
+        for first, count in buckets:            # the owner rule applies per range
+            off, ln = gdraa.gdraa_shard(N, r, count)
+            vmask[first + off:first + off + ln] = True
+        compare(vh[vmask], v_exp[vmask], "f32", what=f"bucketed v N={N} r{r}")
+        assert np.array_equal(vh[~vmask].view(np.uint32), v0[~vmask].view(np.uint32))
+    # the mixed-precision form on the same buckets
+    w_exp2, v_exp2, m_exp = oracle.sgd_step_wd(gs, w0, v0, synth.PAPER_LR, synth.PAPER_MOM,
+                                               wd, model_dtype=oracle.BF16)
+    wm_d = [to_dev(w0) for _ in range(N)]
+    v_d = [to_dev(v0) for _ in range(N)]
+    model_d = [torch.zeros(L, dtype=torch.bfloat16, device=DEV) for _ in range(N)]
+    for first, count in buckets:
+        gdraa.gdraa_vr_sgd_step_mp_range(wm_d, model_d, g_d, v_d, first, count, synth.PAPER_LR,
+                                         synth.PAPER_MOM, wd)
+    torch.cuda.synchronize()
+    for r in range(N):
+        compare(from_dev(model_d[r]), m_exp, "bf16", what=f"bucketed mp model N={N} r{r}")
+        wm, vmask = from_dev(wm_d[r]), np.zeros(L, bool)
+        for first, count in buckets:
+            off, ln = gdraa.gdraa_shard(N, r, count)
+            vmask[first + off:first + off + ln] = True
+        compare(wm[vmask], w_exp2[vmask], "f32", what=f"bucketed mp master N={N} r{r}")
+        compare(from_dev(v_d[r])[vmask], v_exp2[vmask], "f32", what=f"bucketed mp v r{r}")
+    # allreduce_mean on the same buckets
+    bufs = [to_dev(g, bf16) for g in gs]
+    for first, count in buckets:
+        gdraa.gdraa_vr_allreduce_mean_range(bufs, first, count)
+    torch.cuda.synchronize()
+    m_exp = oracle.allreduce_mean(gs)
+    for r in range(N):
+        compare(from_dev(bufs[r]), m_exp, dt, what=f"bucketed mean N={N} r{r}")
+
+
+def test_vr_range_rejects_bad_ranges():
+    N, L = 2, 1000
+    w = [torch.zeros(L, device=DEV) for _ in range(N)]
+    g = [torch.zeros(L, device=DEV) for _ in range(N)]
+    v = [torch.zeros(L, device=DEV) for _ in range(N)]
+    for bad in [(1, 10), (4, 10), (0, 0), (992, 9), (1000, 8)]:
+        with pytest.raises(gdraa.GdraaError) as e:
+            gdraa.gdraa_vr_sgd_step_range(w, g, v, bad[0], bad[1], 0.1, 0.9)
+        assert e.value.name == "GDRAA_EINVAL", bad

@@ -116,6 +116,54 @@ def test_dead_rank_detected(sock):
     assert rc != 0 and "rank 1" in stats["error"]
 
 
+def test_pre_hello_connection_does_not_abort(sock):
+    """A connection that closes before HELLO (readiness probe, stale rank of an earlier
+    job) is not a rank: the job goes on and ends cleanly."""
+    import socket as s
+    world = 2
+    proc = jobserver.start(world, sock)
+    a = FakeRank(sock, 0, world)                   # waits until the server is up
+    probe = s.socket(s.AF_UNIX, s.SOCK_STREAM)
+    probe.connect(sock)
+    probe.close()                                   # connect + close, no HELLO
+    b = FakeRank(sock, 1, world)
+    a.hello()
+    b.hello()
+    name, _, _ = a.expect_hello_ok()
+    b.expect_hello_ok()
+    a.register(1, 10, 0, bytes(64))
+    b.register(1, 10, 0, bytes(64))
+    assert a.recv_reg()[0] == "ok" and b.recv_reg()[0] == "ok"
+    assert read_page(name)["abort"] == 0
+    a.send(6)
+    b.send(6)
+    assert a.recv()[0] == 7 and b.recv()[0] == 7
+    stats, rc = _finish(proc)
+    assert rc == 0 and stats["ok"] and stats["data_bytes"] == 0
+
+
+def test_data_bytes_counts_non_control_payload(sock):
+    """data_bytes is a guard, not a constant: a message outside the control vocabulary
+    (here a would-be 4 KiB tensor payload) is counted and its sender dropped, which
+    fails the job for every rank (the job server moves no weight data)."""
+    world = 2
+    proc = jobserver.start(world, sock)
+    a, b = FakeRank(sock, 0, world), FakeRank(sock, 1, world)
+    a.hello()
+    b.hello()
+    name, _, _ = a.expect_hello_ok()
+    b.expect_hello_ok()
+    b.send(42, bytes(4096))                         # not a control message
+    kind, _, _ = a.recv()
+    assert kind == FAIL
+    page = read_page(name)
+    assert page["data_bytes"] == 4096 and page["abort"] == 1 and page["dead_rank"] == 1
+    a.sock.close()
+    b.sock.close()
+    stats, rc = _finish(proc)
+    assert rc != 0 and stats["data_bytes"] == 4096
+
+
 def test_go_done_page(sock):
     """The shared page the kernels write done[r] into (S:95 IterDone); in gated mode
     the job server raises go[r] = min(done) + 1 (IterStart)."""

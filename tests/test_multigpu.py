@@ -105,7 +105,10 @@ def _worker(rank, world, sock, L_list, out_dir):
             small += 2 * step_mp + 2 * step                    # mp and ex, both families
     assert st["ll_calls"] == small, (st, small)
     assert st["sync_waits"] == 2 * (calls - st["ll_calls"]), st
+    # a0: the kernel's last CTA wrote IterDone = calls completed into the job server's page
+    assert st["iter_done"] == calls, (st, calls)
     report["stats"] = st
+    report["calls"] = calls
     gdraa.gdraa_finalize()
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
         json.dump(report, f)
@@ -125,9 +128,66 @@ def test_multiprocess_parity(tmp_path):
     line = json.loads(out.strip().splitlines()[-1])["jobserver"]
     assert line["ok"] and line["data_bytes"] == 0, line
     assert line["ranks_joined"] == world
-    for r in range(world):
-        rep = json.load(open(tmp_path / f"rank{r}.json"))
+    reps = [json.load(open(tmp_path / f"rank{r}.json")) for r in range(world)]
+    for rep in reps:
         assert rep["cases"] == len(L_list) * 4
+    # the job server saw every rank's IterDone reach the number of calls
+    assert line["done"] == [reps[0]["calls"]] * world, line
+
+
+def _gated_worker(rank, world, sock, out_dir):
+    """Gated mode (IterStart): every call waits on the host until the job server
+    raised go[rank] to its call number, i.e. until every rank finished the previous call.
+    Mixed small (LL) and two-shot steps, chained; bit-exact against the oracle."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    import synth
+    from paper_1802_02326_b200 import gdraa
+    from tests._parity import compare
+    from tests.test_gpu_parity import from_dev, make_grads, to_dev
+
+    torch.cuda.set_device(rank)
+    dev = f"cuda:{rank}"
+    os.environ["GDRAA_JOBSERVER"] = sock
+    gdraa.gdraa_init(world, rank)
+    calls = 0
+    for L in (1000, 1 << 20, 3_000_017):
+        gs = make_grads("like", 71, world, L, False)
+        w0, v0 = synth.w_like(71, L), np.zeros(L, np.float32)
+        g = to_dev(gs[rank], dev=dev)
+        w, v = to_dev(w0, dev=dev), to_dev(v0, dev=dev)
+        gdraa.gdraa_register(w)
+        gdraa.gdraa_register(g)
+        off, ln = gdraa.gdraa_shard(world, rank, L)
+        for it in range(4):
+            w0, v0 = oracle.sgd_step(gs, w0, v0, 0.1, 0.9)
+            gdraa.gdraa_sgd_step(w, g, v, 0.1, 0.9)
+            calls += 1
+            st = gdraa.gdraa_get_stats()           # synchronises: IterDone of this call
+            assert st["iter_done"] == calls and st["iter_start"] >= calls, (st, calls)
+        compare(from_dev(w), w0, "f32", what=f"gated w L={L} r{rank}")
+        compare(from_dev(v)[off:off + ln], v0[off:off + ln], "f32", what=f"gated v r{rank}")
+        gdraa.gdraa_deregister(w)
+        gdraa.gdraa_deregister(g)
+    gdraa.gdraa_finalize()
+    with open(os.path.join(out_dir, f"gated{rank}.json"), "w") as f:
+        json.dump({"calls": calls}, f)
+
+
+def test_multiprocess_gated(tmp_path):
+    from paper_1802_02326_b200 import jobserver
+    world = min(torch.cuda.device_count(), 8)
+    sock = str(tmp_path / "js.sock")
+    js = jobserver.start(world, sock, gated=True)
+    try:
+        mp.start_processes(_gated_worker, args=(world, sock, str(tmp_path)), nprocs=world,
+                           join=True, start_method="spawn")
+    finally:
+        out, err = js.communicate(timeout=120)
+    line = json.loads(out.strip().splitlines()[-1])["jobserver"]
+    calls = [json.load(open(tmp_path / f"gated{r}.json"))["calls"] for r in range(world)]
+    assert line["ok"] and line["data_bytes"] == 0 and line["done"] == calls, line
 
 
 BUCKETS = [(600_000, 400_000), (0, 600_000), (1_000_000, 48_576)]   # backward order

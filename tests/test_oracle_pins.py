@@ -127,6 +127,39 @@ def _exact_expected(cols, N):
     return m
 
 
+def test_mean_bf16_output_rne_ties():
+    # AMB-13 / P:169: allreduce_mean on a bf16 buffer stores bf16_rne(fp32 mean).  N = 2,
+    # bf16 inputs whose exact mean lands on a bf16 rounding tie: 1+2^-8 rounds to even
+    # 1.0 (0x3F80), 1+3*2^-8 rounds to even 1.015625 (0x3F82; truncation gives 0x3F81).
+    a = np.array([0x3F80, 0x3F81, 0xBF81], dtype=np.uint16)      # 1, 1+2^-7, -(1+2^-7)
+    b = np.array([0x3F81, 0x3F82, 0xBF82], dtype=np.uint16)      # 1+2^-7, 1+2^-6, -(1+2^-6)
+    got = oracle.allreduce_mean([a, b])
+    assert got.tolist() == [0x3F80, 0x3F82, 0xBF82]
+
+
+@pytest.mark.parametrize("N", [2, 3, 5])
+def test_mean_bf16_output_matches_torch_cast_of_exact_mean(N):
+    # bf16 inputs with a small exponent spread, so the fp32 left fold is exact; the fp32
+    # mean is then the correctly rounded exact mean (fraction_to_f32), and the stored
+    # bf16 is torch's fp32 -> bf16 cast of it (a library routine).  Near-ties and exact
+    # ties both occur; a truncating or ties-away cast fails.
+    rng = np.random.default_rng(40 + N)
+    L = 3000
+    sig = rng.integers(0x80, 0x100, size=(N, L))                  # 8-bit significands
+    ex = rng.integers(125, 129, size=(N, L))                      # exponents 2^-2 .. 2^1
+    sg = rng.integers(0, 2, size=(N, L))
+    sg[:, : L // 2] = 0                                            # half same-sign
+    bits = ((sg << 15) | (ex << 7) | (sig & 0x7F)).astype(np.uint16)
+    got = oracle.allreduce_mean([bits[p] for p in range(N)])
+    vals = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).float().numpy()
+    means = np.array([fraction_to_f32(sum(exact(vals[p, i]) for p in range(N)) / N)
+                      for i in range(L)], dtype=F32)
+    ref = torch.from_numpy(means).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(got, ref)
+    # the case set really contains values that truncation would get wrong
+    assert np.count_nonzero((means.view(np.uint32) >> 16).astype(np.uint16) != ref) > L // 10
+
+
 @pytest.mark.parametrize("N", [1, 2, 3, 4])
 def test_mean_bruteforce_exact(N):
     # Brute force over a tiny value set: every partial sum of these dyadics is exact in
