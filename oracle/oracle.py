@@ -4,6 +4,7 @@ Argument marshalling only: all arithmetic is in gdraa_oracle.c.  Arrays are nump
 fp32 buffers as float32, bf16 buffers as their raw uint16 bit patterns.
 """
 import ctypes
+import os
 
 import numpy as np
 
@@ -22,7 +23,9 @@ def lib_path() -> str:
 def _load():
     global _lib
     if _lib is None:
-        path = _build.build()
+        # GDRAA_ORACLE_LIB: a separately built copy (tools/oracle_mutations.py loads
+        # deliberately broken builds through it to check that the pins catch them)
+        path = os.environ.get("GDRAA_ORACLE_LIB") or _build.build()
         lib = ctypes.CDLL(path)
         u64, i32, f32 = ctypes.c_uint64, ctypes.c_int, ctypes.c_float
         pu64 = ctypes.POINTER(u64)

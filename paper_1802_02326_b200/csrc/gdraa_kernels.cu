@@ -201,12 +201,18 @@ template <> struct Elem<__nv_bfloat16> {
 };
 
 // Aggregation: s = x_0; s = fl(s + x_p) for p = 1..N-1; m = fl(s / N).
+// For N a power of two, fl(s / N) and fl(s * 2^-k) round the same real number s * 2^-k
+// once, so they are the same bits; the multiply avoids __fdiv_rn's reciprocal
+// refinement (FFMA) and its slow-path call.  Other N: one correctly rounded division.
 template <int WORLD>
 __device__ __forceinline__ float average(const float (&x)[WORLD]) {
     float s = x[0];
 #pragma unroll
     for (int q = 1; q < WORLD; ++q) s = __fadd_rn(s, x[q]);
-    return __fdiv_rn(s, static_cast<float>(WORLD));
+    if constexpr ((WORLD & (WORLD - 1)) == 0)
+        return __fmul_rn(s, 1.0f / static_cast<float>(WORLD));
+    else
+        return __fdiv_rn(s, static_cast<float>(WORLD));
 }
 
 // Update: v = fl(fl(mom*v) + m); w = fl(w - fl(lr*v)).  With weight decay
