@@ -76,7 +76,7 @@ struct KParams {
 enum Mode { kMean = 0, kSgd = 1, kSgdMp = 2 };
 
 // KParams::flags.  kFlagCtaFence: at exit, one fence.acq_rel.sys per CTA after
-// __syncthreads() instead of one per thread (GDRAA_EXIT_FENCE=cta|thread).
+// __syncthreads() instead of one per thread (default; GDRAA_EXIT_FENCE=thread clears it).
 constexpr uint32_t kFlagCtaFence = 1u;
 uint32_t env_kernel_flags();
 constexpr int kModes = 3;

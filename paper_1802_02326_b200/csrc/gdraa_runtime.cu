@@ -411,10 +411,14 @@ struct VrDevice {
 
 }  // namespace
 
+// Kernel variant switches.  Exit fence: one fence.acq_rel.sys per CTA after
+// __syncthreads() (default) -- measured 6-7 us faster per call than one per thread at
+// R50 (N = 2: 166.5 -> 160.0 us, N = 4: 244.1 -> 237.3 us; profiles/r62_fence_ab.json);
+// GDRAA_EXIT_FENCE=thread restores the per-thread fence for A/B runs.
 uint32_t env_kernel_flags() {
     static const uint32_t v = [] {
         const char *e = std::getenv("GDRAA_EXIT_FENCE");
-        return (e != nullptr && std::strcmp(e, "cta") == 0) ? kFlagCtaFence : 0u;
+        return (e != nullptr && std::strcmp(e, "thread") == 0) ? 0u : kFlagCtaFence;
     }();
     return v;
 }

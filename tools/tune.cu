@@ -6,12 +6,14 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
 //        -o tools/tune tools/tune.cu
-//   ./tools/tune <world> <L> <f32|bf16> <sgd|mean> [iters] [lib|lsu|tma|ctas]
+//   ./tools/tune <world> <L> <f32|bf16> <sgd|mp|mean> [iters] [lib|lsu|tma|tail|ctas|solo]
 //     lib : the library's launch shapes (LSU and TMA kernels)
 //     lsu : sweep of the LSU kernel's (U, threads, CTAs/SM)
 //     tma : sweep of the TMA kernel's (consumer warps, stages)
 //     tail: end-game variants of the TMA kernel (small-chunk size, in-flight depth)
 //     ctas: both kernels at grid caps 16/32/64/all (how many SMs the collective needs)
+//     solo: the library shapes with rank 0 alone (barriers pre-satisfied): one rank's
+//           NVLink traffic in one direction pair, and a kernel ncu can replay
 #define GDRAA_TRACE 1
 #include "../paper_1802_02326_b200/csrc/gdraa_kernels.cu"
 
@@ -36,6 +38,7 @@ using namespace gdraa;
 struct Bufs {
     void *g[3];
     float *w[3], *v[3];
+    void *model[3];   // bf16 model copy (mode mp: the all-gathered buffer; w is the master)
     Pad *pad;
 };
 
@@ -47,6 +50,11 @@ static std::string WHAT = "lsu";
 static std::vector<Bufs> B;
 static ErrBlock *err_d;
 static std::vector<uint64_t *> TR;   // per-device trace ring (64 calls x 8 vr x 8 stamps)
+// solo: only device 0 (rank 0) runs; its pad's entry/exit slots are pre-set past every
+// epoch, so both barriers pass at once and the kernel moves rank 0's NVLink traffic alone
+// (no kernel waits on another GPU: ncu kernel replay works on it).
+static bool SOLO = false;
+static uint32_t FLAGS = kFlagCtaFence;
 
 // Time `fn` (grid gx x threads, dynamic smem) on all W devices; print one line.
 template <typename TG, int WORLD, int MODE>
@@ -65,8 +73,9 @@ void run(void (*fn)(KParams), int threads, int smem, int gx, const char *kernel,
         CK(cudaEventCreate(&e0[d]));
         CK(cudaEventCreate(&e1[d]));
     }
+    const int active = SOLO ? 1 : WORLD;
     auto launch = [&](int set) {
-        for (int d = 0; d < WORLD; ++d) {
+        for (int d = 0; d < active; ++d) {
             KParams p;
             std::memset(&p, 0, sizeof p);
             p.world = WORLD;
@@ -78,10 +87,15 @@ void run(void (*fn)(KParams), int threads, int smem, int gx, const char *kernel,
             p.timeout_ns = 10ull * 1000000000ull;
             for (int q = 0; q < WORLD; ++q) {
                 p.src[0][q] = B[q].g[set];
-                p.dst[0][q] = MODE == kSgd ? (void *)B[q].w[set] : B[q].g[set];
+                p.dst[0][q] = MODE == kSgd   ? (void *)B[q].w[set]
+                              : MODE == kSgdMp ? B[q].model[set]
+                                               : B[q].g[set];
                 p.pad[0][q] = B[q].pad;
             }
             p.v[0] = B[d].v[set];
+            p.wm[0] = MODE == kSgdMp ? B[d].w[set] : nullptr;
+            p.wd = MODE == kSgdMp ? 0.001f : 0.0f;
+            p.flags = FLAGS;
             p.err = err_d;
             p.trace = TR[d];
             CK(cudaSetDevice(d));
@@ -91,10 +105,10 @@ void run(void (*fn)(KParams), int threads, int smem, int gx, const char *kernel,
     };
     for (int i = 0; i < 5; ++i) launch(i % 3);
     for (int d = 0; d < WORLD; ++d) { CK(cudaSetDevice(d)); CK(cudaDeviceSynchronize()); }
-    for (int d = 0; d < WORLD; ++d) { CK(cudaSetDevice(d)); CK(cudaEventRecord(e0[d], st[d])); }
+    for (int d = 0; d < active; ++d) { CK(cudaSetDevice(d)); CK(cudaEventRecord(e0[d], st[d])); }
     for (int i = 0; i < ITERS; ++i) launch(i % 3);
     float worst = 0;
-    for (int d = 0; d < WORLD; ++d) {
+    for (int d = 0; d < active; ++d) {
         CK(cudaSetDevice(d));
         CK(cudaEventRecord(e1[d], st[d]));
         CK(cudaEventSynchronize(e1[d]));
@@ -110,7 +124,7 @@ void run(void (*fn)(KParams), int threads, int smem, int gx, const char *kernel,
     // 3 last CTA arrived (after its fence), 4 exit barrier passed
     double acc[6] = {0, 0, 0, 0, 0, 0};
     int cnt = 0;
-    for (int d = 0; d < WORLD; ++d) {
+    for (int d = 0; d < active; ++d) {
         std::vector<uint64_t> h(64 * kMaxWorld * 8);
         CK(cudaSetDevice(d));
         CK(cudaMemcpy(h.data(), TR[d], h.size() * 8, cudaMemcpyDeviceToHost));
@@ -130,15 +144,19 @@ void run(void (*fn)(KParams), int threads, int smem, int gx, const char *kernel,
     }
     const double t = worst / ITERS * 1e-3;
     const int sg = sizeof(TG);
-    const double bytes = WORLD == 1 ? (MODE == kSgd ? (sg + 16.0) * L : 2.0 * sg * L)
-                                    : (WORLD - 1.0) / WORLD * L * (sg + (MODE == kSgd ? 4 : sg));
+    const double sw = MODE == kSgd ? 4 : (MODE == kSgdMp ? 2 : sg);
+    const double bytes = WORLD == 1 ? (MODE == kMean ? 2.0 * sg * L
+                                                     : (sg + 16.0 + (MODE == kSgdMp ? 2 : 0)) * L)
+                                    : (WORLD - 1.0) / WORLD * L * (sg + sw);
     auto ph = [&](int k) { return cnt ? acc[k] / cnt / 1e3 : 0.0; };
     std::printf("{\"world\": %d, \"L\": %zu, \"dtype\": \"%s\", \"mode\": \"%s\", \"kernel\": "
                 "\"%s\", \"shape\": \"%s\", \"threads\": %d, \"smem\": %d, \"grid\": %d, "
                 "\"us\": %.2f, \"gbs_per_rank\": %.1f, \"phase_us\": {\"entry\": %.2f, "
                 "\"data_first_cta\": %.2f, \"cta_spread\": %.2f, \"drain\": %.2f, "
                 "\"exit\": %.2f, \"gap_to_next\": %.2f}}\n",
-                WORLD, L, sg == 4 ? "f32" : "bf16", MODE == kSgd ? "sgd" : "mean", kernel,
+                WORLD, L, sg == 4 ? "f32" : "bf16",
+                MODE == kSgd ? "sgd" : (MODE == kSgdMp ? "mp" : "mean"),
+                SOLO ? (std::string(kernel) + "_solo").c_str() : kernel,
                 shape.c_str(), threads, smem, gx, t * 1e6, bytes / t / 1e9, ph(0), ph(1), ph(2),
                 ph(3), ph(4), ph(5));
     std::fflush(stdout);
@@ -242,15 +260,21 @@ void dispatch_world() {
 
 int main(int argc, char **argv) {
     if (argc < 5) {
-        std::fprintf(stderr, "usage: tune <world> <L> <f32|bf16> <sgd|mean> [iters] [lib|lsu|tma|tail|ctas]\n");
+        std::fprintf(stderr, "usage: tune <world> <L> <f32|bf16> <sgd|mp|mean> [iters] [lib|lsu|tma|tail|ctas|solo]\n");
         return 1;
     }
     W = std::atoi(argv[1]);
     L = std::strtoull(argv[2], nullptr, 10);
     DT = std::string(argv[3]) == "bf16" ? GDRAA_BF16 : GDRAA_F32;
-    MODE_ = std::string(argv[4]) == "mean" ? kMean : kSgd;
+    MODE_ = std::string(argv[4]) == "mean" ? kMean : (std::string(argv[4]) == "mp" ? kSgdMp : kSgd);
+    if (const char *f = std::getenv("GDRAA_EXIT_FENCE"))
+        FLAGS = std::strcmp(f, "thread") == 0 ? 0u : kFlagCtaFence;
     if (argc > 5) ITERS = std::atoi(argv[5]);
     if (argc > 6) WHAT = argv[6];
+    if (WHAT == "solo") {
+        SOLO = true;
+        WHAT = "lib";
+    }
     CK(cudaGetDeviceCount(&NDEV));
     if (NDEV < W) {
         std::fprintf(stderr, "need %d GPUs, have %d\n", W, NDEV);
@@ -266,12 +290,20 @@ int main(int argc, char **argv) {
             CK(cudaMalloc(&B[d].g[s], gb));
             CK(cudaMalloc(&B[d].w[s], L * 4));
             CK(cudaMalloc(&B[d].v[s], L * 4));
+            CK(cudaMalloc(&B[d].model[s], L * 2));
+            CK(cudaMemset(B[d].model[s], 0, L * 2));
             CK(cudaMemset(B[d].g[s], 0, gb));
             CK(cudaMemset(B[d].w[s], 0, L * 4));
             CK(cudaMemset(B[d].v[s], 0, L * 4));
         }
         CK(cudaMalloc(&B[d].pad, sizeof(Pad)));
         CK(cudaMemset(B[d].pad, 0, sizeof(Pad)));
+        if (SOLO && d == 0) {   // every peer "has arrived" at every epoch
+            Pad h;
+            std::memset(&h, 0, sizeof h);
+            for (int q = 0; q < kMaxWorld; ++q) h.entry[q] = h.exit[q] = 1ull << 60;
+            CK(cudaMemcpy(B[d].pad, &h, sizeof h, cudaMemcpyHostToDevice));
+        }
         uint64_t *tr;
         CK(cudaMalloc(&tr, 64 * kMaxWorld * 8 * 8));
         CK(cudaMemset(tr, 0, 64 * kMaxWorld * 8 * 8));
@@ -282,9 +314,13 @@ int main(int argc, char **argv) {
     std::memset(eh, 0, sizeof(ErrBlock));
     err_d = (ErrBlock *)eh;   // UVA: the host pointer is valid on the device
     if (DT == GDRAA_F32) {
-        if (MODE_ == kSgd) dispatch_world<float, kSgd>(); else dispatch_world<float, kMean>();
+        if (MODE_ == kSgd) dispatch_world<float, kSgd>();
+        else if (MODE_ == kSgdMp) dispatch_world<float, kSgdMp>();
+        else dispatch_world<float, kMean>();
     } else {
-        if (MODE_ == kSgd) dispatch_world<__nv_bfloat16, kSgd>(); else dispatch_world<__nv_bfloat16, kMean>();
+        if (MODE_ == kSgd) dispatch_world<__nv_bfloat16, kSgd>();
+        else if (MODE_ == kSgdMp) dispatch_world<__nv_bfloat16, kSgdMp>();
+        else dispatch_world<__nv_bfloat16, kMean>();
     }
     return 0;
 }
