@@ -28,7 +28,8 @@ struct alignas(128) Pad {
     uint32_t arrive;               // CTA arrival counter of the running call
     uint32_t next;                 // next work chunk of the running call (dynamic schedule)
     uint64_t ll_calls;             // calls served by the small-message (LL) path
-    uint64_t _p3[11];
+    uint64_t mc_calls;             // calls that used the multicast barrier (tools/tune.cu A/B)
+    uint64_t _p3[10];
 };
 static_assert(sizeof(Pad) % 128 == 0, "pad layout");
 
@@ -66,6 +67,14 @@ struct KParams {
     const volatile int32_t *abort;           // host-mapped job-server abort flag, or null:
                                              // spins give up early once a rank has died
     uint32_t flags;                          // kFlag* bits (launch-variant switches)
+    // NVLS multicast variants of the two-shot TMA kernel (set only by
+    // tools/tune.cu for the A/B, null in the library): mc_dst[vr] = multicast VA of the
+    // broadcast buffer (one multimem.st reaches every member of the group); mc_bar[vr] =
+    // multicast VA of a {entry, exit} u64 counter block whose local copy is bar_local[vr]
+    // (one multimem.red per rank and barrier instead of N-1 flag stores).
+    void *mc_dst[kMaxWorld];
+    uint64_t *mc_bar[kMaxWorld];
+    uint64_t *bar_local[kMaxWorld];
 #ifdef GDRAA_TRACE
     uint64_t *trace;                         // tools/tune.cu only: %globaltimer stamps
 #endif
@@ -78,6 +87,9 @@ enum Mode { kMean = 0, kSgd = 1, kSgdMp = 2 };
 // KParams::flags.  kFlagCtaFence: at exit, one fence.acq_rel.sys per CTA after
 // __syncthreads() instead of one per thread (default; GDRAA_EXIT_FENCE=thread clears it).
 constexpr uint32_t kFlagCtaFence = 1u;
+// kFlagMcPeersOnly: the mc_dst group holds the N-1 peers only; the own copy is stored
+// locally as well.
+constexpr uint32_t kFlagMcPeersOnly = 2u;
 uint32_t env_kernel_flags();
 constexpr int kModes = 3;
 

@@ -51,6 +51,36 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// NVLS multicast (the address is a multicast VA: the switch delivers to every member).
+__device__ __forceinline__ void mc_st(uint4 *p, uint4 v) {
+    asm volatile("multimem.st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(__uint_as_float(v.x)),
+                 "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
+                 : "memory");
+}
+__device__ __forceinline__ void mc_st(uint2 *p, uint2 v) {
+    asm volatile("multimem.st.global.v2.bf16x2 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y)
+                 : "memory");
+}
+__device__ __forceinline__ void mc_st_bf16(uint2 *p, uint2 v) { mc_st(p, v); }
+__device__ __forceinline__ void mc_st_bf16(uint4 *p, uint4 v) {
+    asm volatile("multimem.st.global.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+// The h-th 8-byte half of a bf16 output vector (4 or 8 values).
+__device__ __forceinline__ void set_half(uint2 &o, int, uint2 v) { o = v; }
+__device__ __forceinline__ void set_half(uint4 &o, int h, uint2 v) {
+    if (h == 0) {
+        o.x = v.x;
+        o.y = v.y;
+    } else {
+        o.z = v.x;
+        o.w = v.y;
+    }
+}
+__device__ __forceinline__ void mc_red_add_release(uint64_t *p, uint64_t v) {
+    asm volatile("multimem.red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void fence_acq_rel_sys() {
     asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
@@ -209,7 +239,9 @@ __device__ __forceinline__ float average(const float (&x)[WORLD]) {
     float s = x[0];
 #pragma unroll
     for (int q = 1; q < WORLD; ++q) s = __fadd_rn(s, x[q]);
-    if constexpr ((WORLD & (WORLD - 1)) == 0)
+    if constexpr (WORLD == 1)
+        return s;                                   // fl(s / 1) = s
+    else if constexpr ((WORLD & (WORLD - 1)) == 0)
         return __fmul_rn(s, 1.0f / static_cast<float>(WORLD));
     else
         return __fdiv_rn(s, static_cast<float>(WORLD));
@@ -871,14 +903,22 @@ struct TmaCfg {
     static constexpr int SMEM = STAGES * STAGE_BYTES;
 };
 
+// VE_: elements per consumer thread per step (0 = 8 when the broadcast is bf16 -- the bf16
+// mean and the mixed-precision model copy -- so that every destination gets one 16-byte
+// store per thread and step, else 4).
 template <typename TG, int WORLD, int MODE, int CW_ = 16, int ST_ = 4, int TAILDIV_ = 4,
-          int TDEPTH_ = ST_, int ROT_ = 0>
+          int TDEPTH_ = ST_, int ROT_ = 0, int VE_ = 0>
 __global__ void __launch_bounds__(TmaCfg<TG, WORLD, MODE, CW_, ST_, TAILDIV_, TDEPTH_, ROT_>::THREADS, 1)
 gdraa_tma_kernel(const __grid_constant__ KParams p) {
     using C = TmaCfg<TG, WORLD, MODE, CW_, ST_, TAILDIV_, TDEPTH_, ROT_>;
     using EL = Elem<TG>;
     using Raw = typename EL::Raw;
     constexpr bool kUpdate = C::UPD;
+    constexpr bool kBfOut = MODE == kSgdMp || (MODE == kMean && !std::is_same<TG, float>::value);
+    constexpr int VE = VE_ != 0 ? VE_ : (kBfOut ? 8 : 4);
+    constexpr int H = VE / E;                 // 4-element vectors per thread and step
+    static_assert(H == 1 || (H == 2 && kBfOut), "VE = 8 only for bf16 broadcasts");
+    using BfOut = typename std::conditional<H == 2, uint4, uint2>::type;   // VE bf16 values
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t full[C::STAGES], empty[C::STAGES];
     __shared__ uint32_t s_chunk[C::STAGES];
@@ -898,8 +938,19 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP_START();
+    // multicast barrier variant: counters reach (mc_calls + 1) * N once every rank arrived
+    const bool mcb = WORLD > 1 && p.mc_bar[vr] != nullptr;
+    const uint64_t mc_target =
+        mcb ? (*reinterpret_cast<volatile uint64_t *>(&mine->mc_calls) + 1) * WORLD : 0;
     // a2: "2nd synchronization"
-    if (WORLD > 1) {
+    if (WORLD > 1 && mcb) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) mc_red_add_release(p.mc_bar[vr], 1);
+        __syncthreads();
+        if (threadIdx.x == 0 && !wait_geq(p.bar_local[vr], mc_target, p.timeout_ns, p.abort)) {
+            report_timeout(p.err, 1, rank, vr);
+            s_abort = 1;
+        }
+    } else if (WORLD > 1) {
         if (blockIdx.x == 0 && threadIdx.x < WORLD && threadIdx.x != rank)
             st_release_sys(&p.pad[vr][threadIdx.x]->entry[rank], epoch);
         __syncthreads();
@@ -988,6 +1039,8 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     } else {
         // consumers: a4 fold (+ a5 update) from shared memory, a6 push
         const int ct = threadIdx.x - 32;
+        void *const mcd = WORLD > 1 ? p.mc_dst[vr] : nullptr;   // multicast broadcast (A/B)
+        const bool mc_self = (p.flags & kFlagMcPeersOnly) != 0;
         for (uint32_t it = 0;; ++it) {
             const int s = it % C::STAGES;
             mbar_wait(&full[s], (it / C::STAGES) & 1);
@@ -996,51 +1049,88 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
             uint64_t e0;
             uint32_t n_el;
             chunk(c, e0, n_el);
-            for (uint32_t k = ct * E; k < n_el; k += C::CW * 32 * E) {
-                float x[WORLD][E];
+            for (uint32_t k = ct * VE; k < n_el; k += C::CW * 32 * VE) {
+                float m[H][E];
 #pragma unroll
-                for (int q = 0; q < WORLD; ++q)
-                    EL::widen(*reinterpret_cast<const Raw *>(stage_src(s, q) + k), x[q]);
-                float m[E];
+                for (int h = 0; h < H; ++h) {
+                    float x[WORLD][E];
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    float col[WORLD];
+                    for (int q = 0; q < WORLD; ++q)
+                        EL::widen(*reinterpret_cast<const Raw *>(stage_src(s, q) + k + h * E), x[q]);
 #pragma unroll
-                    for (int q = 0; q < WORLD; ++q) col[q] = x[q][e];
-                    m[e] = average<WORLD>(col);
+                    for (int e = 0; e < E; ++e) {
+                        float col[WORLD];
+#pragma unroll
+                        for (int q = 0; q < WORLD; ++q) col[q] = x[q][e];
+                        m[h][e] = average<WORLD>(col);
+                    }
                 }
                 const uint64_t g0 = off + e0 + k;
                 if (kUpdate) {
-                    float4 w = *reinterpret_cast<const float4 *>(stage_w(s) + k);
-                    float4 v = *reinterpret_cast<const float4 *>(stage_v(s) + k);
-                    sgd(m[0], lr, mom, wd, w.x, v.x);
-                    sgd(m[1], lr, mom, wd, w.y, v.y);
-                    sgd(m[2], lr, mom, wd, w.z, v.z);
-                    sgd(m[3], lr, mom, wd, w.w, v.w);
-                    st_vec(reinterpret_cast<uint4 *>(vloc + g0), as_u4(v.x, v.y, v.z, v.w));
+                    float4 w[H];
+#pragma unroll
+                    for (int h = 0; h < H; ++h) {
+                        w[h] = *reinterpret_cast<const float4 *>(stage_w(s) + k + h * E);
+                        float4 v = *reinterpret_cast<const float4 *>(stage_v(s) + k + h * E);
+                        sgd(m[h][0], lr, mom, wd, w[h].x, v.x);
+                        sgd(m[h][1], lr, mom, wd, w[h].y, v.y);
+                        sgd(m[h][2], lr, mom, wd, w[h].z, v.z);
+                        sgd(m[h][3], lr, mom, wd, w[h].w, v.w);
+                        st_vec(reinterpret_cast<uint4 *>(vloc + g0 + h * E), as_u4(v.x, v.y, v.z, v.w));
+                    }
                     if (MODE == kSgd) {
-                        const uint4 o = as_u4(w.x, w.y, w.z, w.w);
 #pragma unroll
-                        for (int j = 1; j <= WORLD; ++j) {
-                            const int q = (rank + j) % WORLD;
-                            st_vec(reinterpret_cast<uint4 *>(static_cast<float *>(p.dst[vr][q]) + g0), o);
+                        for (int h = 0; h < H; ++h) {
+                            const uint4 o = as_u4(w[h].x, w[h].y, w[h].z, w[h].w);
+                            const uint64_t gh = g0 + h * E;
+                            if (mcd != nullptr) {
+                                mc_st(reinterpret_cast<uint4 *>(static_cast<float *>(mcd) + gh), o);
+                                if (mc_self)
+                                    st_vec(reinterpret_cast<uint4 *>(static_cast<float *>(p.dst[vr][rank]) + gh), o);
+                            } else {
+#pragma unroll
+                                for (int j = 1; j <= WORLD; ++j) {
+                                    const int q = (rank + j) % WORLD;
+                                    st_vec(reinterpret_cast<uint4 *>(static_cast<float *>(p.dst[vr][q]) + gh), o);
+                                }
+                            }
                         }
-                    } else {
-                        st_vec(reinterpret_cast<uint4 *>(wloc + g0), as_u4(w.x, w.y, w.z, w.w));
-                        const float wf[E] = {w.x, w.y, w.z, w.w};
-                        const uint2 o = Elem<__nv_bfloat16>::narrow(wf);
+                    } else {   // kSgdMp: fp32 master shard stays local, bf16 copy to every rank
+                        BfOut o;
 #pragma unroll
-                        for (int j = 1; j <= WORLD; ++j) {
-                            const int q = (rank + j) % WORLD;
-                            st_vec(reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(p.dst[vr][q]) + g0), o);
+                        for (int h = 0; h < H; ++h) {
+                            st_vec(reinterpret_cast<uint4 *>(wloc + g0 + h * E),
+                                   as_u4(w[h].x, w[h].y, w[h].z, w[h].w));
+                            const float wf[E] = {w[h].x, w[h].y, w[h].z, w[h].w};
+                            set_half(o, h, Elem<__nv_bfloat16>::narrow(wf));
+                        }
+                        if (mcd != nullptr) {
+                            mc_st_bf16(reinterpret_cast<BfOut *>(static_cast<__nv_bfloat16 *>(mcd) + g0), o);
+                            if (mc_self)
+                                st_vec(reinterpret_cast<BfOut *>(static_cast<__nv_bfloat16 *>(p.dst[vr][rank]) + g0), o);
+                        } else {
+#pragma unroll
+                            for (int j = 1; j <= WORLD; ++j) {
+                                const int q = (rank + j) % WORLD;
+                                st_vec(reinterpret_cast<BfOut *>(static_cast<__nv_bfloat16 *>(p.dst[vr][q]) + g0), o);
+                            }
                         }
                     }
-                } else {
-                    const Raw o = EL::narrow(m);
+                } else if constexpr (std::is_same<TG, float>::value) {
+                    const Raw o = EL::narrow(m[0]);
 #pragma unroll
                     for (int j = 1; j <= WORLD; ++j) {
                         const int q = (rank + j) % WORLD;
                         st_vec(reinterpret_cast<Raw *>(static_cast<TG *>(p.dst[vr][q]) + g0), o);
+                    }
+                } else {   // bf16 mean: VE elements -> one store per destination
+                    BfOut o;
+#pragma unroll
+                    for (int h = 0; h < H; ++h) set_half(o, h, EL::narrow(m[h]));
+#pragma unroll
+                    for (int j = 1; j <= WORLD; ++j) {
+                        const int q = (rank + j) % WORLD;
+                        st_vec(reinterpret_cast<BfOut *>(static_cast<TG *>(p.dst[vr][q]) + g0), o);
                     }
                 }
             }
@@ -1091,7 +1181,17 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     __syncthreads();
     if (!s_last) return;
     if (threadIdx.x == 0) GDRAA_STAMP(3);
-    if (WORLD > 1) {
+    if (WORLD > 1 && mcb) {
+        if (threadIdx.x == 0) {
+            mc_red_add_release(p.mc_bar[vr] + 1, 1);
+            if (!wait_geq(p.bar_local[vr] + 1, mc_target, p.timeout_ns, p.abort)) {
+                report_timeout(p.err, 2, rank, vr);
+                s_abort = 1;
+            }
+        }
+        __syncthreads();
+        if (s_abort) return;
+    } else if (WORLD > 1) {
         if (threadIdx.x < WORLD && threadIdx.x != rank)
             st_release_sys(&p.pad[vr][threadIdx.x]->exit[rank], epoch);
         if (threadIdx.x < WORLD && threadIdx.x != rank) {
@@ -1109,6 +1209,7 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
         mine->next = 0;
         mine->calls += 1;
         if (WORLD > 1) mine->sync_waits += 2;
+        if (mcb) mine->mc_calls += 1;
         mine->epoch = epoch;
         if (p.done[vr] != nullptr) *p.done[vr] = epoch;
     }

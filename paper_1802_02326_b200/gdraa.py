@@ -9,7 +9,9 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libgdraa.so")
+# GDRAA_LIB_PATH: load another build of the same library (A/B timing of two builds on one
+# box only); the default is the in-tree build.
+LIB_PATH = os.environ.get("GDRAA_LIB_PATH") or os.path.join(PKG, "lib", "libgdraa.so")
 
 GDRAA_F32 = 0
 GDRAA_BF16 = 1

@@ -22,11 +22,11 @@ DEFAULT_PATH = [
     ("N=1 local fused SGD, fp32 (gdraa_kernel<float,1,kSgd,U1,512,2>)",
      r"12gdraa_kernelIfLi1ELi1ELi1ELi512ELi2EEE"),
     ("N=2 two-shot fused SGD, fp32, TMA-staged (gdraa_tma_kernel<float,2,kSgd>)",
-     r"16gdraa_tma_kernelIfLi2ELi1ELi16ELi4ELi4ELi4ELi0EEE"),
+     r"16gdraa_tma_kernelIfLi2ELi1ELi16ELi4ELi4ELi4ELi0E(Li0E)?EE"),
     ("N=4 two-shot fused SGD, fp32, TMA-staged (gdraa_tma_kernel<float,4,kSgd>)",
-     r"16gdraa_tma_kernelIfLi4ELi1ELi16ELi4ELi4ELi4ELi0EEE"),
+     r"16gdraa_tma_kernelIfLi4ELi1ELi16ELi4ELi4ELi4ELi0E(Li0E)?EE"),
     ("N=4 two-shot mixed-precision SGD, bf16 g (gdraa_tma_kernel<bf16,4,kSgdMp>)",
-     r"16gdraa_tma_kernelI13__nv_bfloat16Li4ELi2ELi16ELi4ELi4ELi4ELi0EEE"),
+     r"16gdraa_tma_kernelI13__nv_bfloat16Li4ELi2ELi16ELi4ELi4ELi4ELi0E(Li0E)?EE"),
     ("N=2 two-shot fused SGD, bf16 g, LSU (gdraa_kernel<bf16,2,kSgd,U2,1024,1>)",
      r"12gdraa_kernelI13__nv_bfloat16Li2ELi1ELi2ELi1024ELi1EEE"),
     ("N=2 small-message SGD, fp32 (gdraa_ll_sgd_kernel<float,2,kSgd>)",

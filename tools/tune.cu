@@ -5,17 +5,20 @@
 // with a per-phase breakdown from %globaltimer stamps (kernels built with GDRAA_TRACE).
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
-//        -o tools/tune tools/tune.cu
+//        -o tools/tune tools/tune.cu -lcuda
 //   ./tools/tune <world> <L> <f32|bf16> <sgd|mp|mean> [iters] [lib|lsu|tma|tail|ctas|solo]
 //     lib : the library's launch shapes (LSU and TMA kernels)
 //     lsu : sweep of the LSU kernel's (U, threads, CTAs/SM)
 //     tma : sweep of the TMA kernel's (consumer warps, stages)
 //     tail: end-game variants of the TMA kernel (small-chunk size, in-flight depth)
 //     ctas: both kernels at grid caps 16/32/64/all (how many SMs the collective needs)
+//     mc  : the TMA kernel with NVLS multicast all-gather and / or barriers (needs -lcuda)
 //     solo: the library shapes with rank 0 alone (barriers pre-satisfied): one rank's
 //           NVLink traffic in one direction pair, and a kernel ncu can replay
 #define GDRAA_TRACE 1
 #include "../paper_1802_02326_b200/csrc/gdraa_kernels.cu"
+
+#include <cuda.h>
 
 #include <cstdio>
 #include <cstdlib>
@@ -25,6 +28,16 @@
 
 using namespace gdraa;
 
+#define CU(x)                                                                            \
+    do {                                                                                 \
+        CUresult r_ = (x);                                                               \
+        if (r_ != CUDA_SUCCESS) {                                                        \
+            const char *s_ = nullptr;                                                    \
+            cuGetErrorString(r_, &s_);                                                   \
+            std::fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, s_ ? s_ : "?"); \
+            std::exit(1);                                                                \
+        }                                                                                \
+    } while (0)
 #define CK(x)                                                                            \
     do {                                                                                 \
         cudaError_t e = (x);                                                             \
@@ -40,6 +53,8 @@ struct Bufs {
     float *w[3], *v[3];
     void *model[3];   // bf16 model copy (mode mp: the all-gathered buffer; w is the master)
     Pad *pad;
+    void *mc_dst[3];  // mc mode: multicast VA of this set's broadcast buffer (w or model)
+    uint64_t *mc_bar, *bar_local;   // mc mode: multicast / local VA of {entry, exit} counters
 };
 
 static int W, NDEV;
@@ -55,6 +70,11 @@ static std::vector<uint64_t *> TR;   // per-device trace ring (64 calls x 8 vr x
 // (no kernel waits on another GPU: ncu kernel replay works on it).
 static bool SOLO = false;
 static uint32_t FLAGS = kFlagCtaFence;
+// mc: NVLS multicast A/B: the broadcast buffers are VMM allocations
+// bound to one multicast object per set (all N devices); MC_AG sends w' with one
+// multimem.st per vector instead of N-1 unicast stores, MC_BAR runs both barriers as one
+// multimem.red per rank.
+static bool MC = false, MC_AG = false, MC_BAR = false;
 
 // Time `fn` (grid gx x threads, dynamic smem) on all W devices; print one line.
 template <typename TG, int WORLD, int MODE>
@@ -94,6 +114,9 @@ void run(void (*fn)(KParams), int threads, int smem, int gx, const char *kernel,
             }
             p.v[0] = B[d].v[set];
             p.wm[0] = MODE == kSgdMp ? B[d].w[set] : nullptr;
+            p.mc_dst[0] = MC_AG ? B[d].mc_dst[set] : nullptr;
+            p.mc_bar[0] = MC_BAR ? B[d].mc_bar : nullptr;
+            p.bar_local[0] = MC_BAR ? B[d].bar_local : nullptr;
             p.wd = MODE == kSgdMp ? 0.001f : 0.0f;
             p.flags = FLAGS;
             p.err = err_d;
@@ -156,7 +179,8 @@ void run(void (*fn)(KParams), int threads, int smem, int gx, const char *kernel,
                 "\"exit\": %.2f, \"gap_to_next\": %.2f}}\n",
                 WORLD, L, sg == 4 ? "f32" : "bf16",
                 MODE == kSgd ? "sgd" : (MODE == kSgdMp ? "mp" : "mean"),
-                SOLO ? (std::string(kernel) + "_solo").c_str() : kernel,
+                (std::string(kernel) + (SOLO ? "_solo" : "") + (MC_AG ? "_mcag" : "") +
+                 (MC_BAR ? "_mcbar" : "")).c_str(),
                 shape.c_str(), threads, smem, gx, t * 1e6, bytes / t / 1e9, ph(0), ph(1), ph(2),
                 ph(3), ph(4), ph(5));
     std::fflush(stdout);
@@ -187,10 +211,11 @@ void lsu(int cap = 0) {
     run<TG, WORLD, MODE>(fn, THREADS, 0, (int)std::max<uint64_t>(gx, 1), "lsu", shape);
 }
 
-template <typename TG, int WORLD, int MODE, int CW, int ST, int TD = 4, int TDEP = ST, int ROT = 0>
+template <typename TG, int WORLD, int MODE, int CW, int ST, int TD = 4, int TDEP = ST, int ROT = 0,
+          int VE = 0>
 void tma(int cap = 0) {
     using C = TmaCfg<TG, WORLD, MODE, CW, ST, TD, TDEP, ROT>;
-    auto fn = gdraa_tma_kernel<TG, WORLD, MODE, CW, ST, TD, TDEP, ROT>;
+    auto fn = gdraa_tma_kernel<TG, WORLD, MODE, CW, ST, TD, TDEP, ROT, VE>;
     CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(fn),
                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     int per = 0;
@@ -201,8 +226,8 @@ void tma(int cap = 0) {
                                      (uint64_t)sm_count() * per);
     if (cap > 0) gx = std::min<uint64_t>(gx, cap);
     char shape[64];
-    std::snprintf(shape, sizeof shape, "CW%d_ST%d_CH%d_TD%d_TDEP%d_ROT%d_per%d", CW, ST, C::CH,
-                  TD, C::TDEPTH, ROT, per);
+    std::snprintf(shape, sizeof shape, "CW%d_ST%d_CH%d_TD%d_TDEP%d_ROT%d_VE%d_per%d", CW, ST,
+                  C::CH, TD, C::TDEPTH, ROT, VE, per);
     run<TG, WORLD, MODE>(fn, C::THREADS, C::SMEM, (int)std::max<uint64_t>(gx, 1), "tma", shape);
 }
 
@@ -239,6 +264,24 @@ void sweep() {
             tma<TG, WORLD, MODE, 16, 4, 4, 4, 1>();
             tma<TG, WORLD, MODE, 16, 4, 8, 2, 1>();
         }
+    } else if (WHAT == "ve") {
+        // bf16 broadcasts: 4 vs 8 elements per consumer thread and step (8-byte vs 16-byte
+        // stores per destination), twice, interleaved
+        if constexpr (MODE == kSgdMp || (MODE == kMean && !std::is_same<TG, float>::value))
+            for (int rep = 0; rep < 2; ++rep) {
+                tma<TG, WORLD, MODE, 16, 4, 4, 4, 0, 4>();
+                tma<TG, WORLD, MODE, 16, 4, 4, 4, 0, 8>();
+            }
+    } else if (WHAT == "mc") {
+        // the library's TMA shape: unicast, multicast all-gather, multicast barriers, both;
+        // twice, interleaved
+        for (int rep = 0; rep < 2; ++rep)
+            for (int v = 0; v < 4; ++v) {
+                MC_AG = (v & 1) != 0;
+                MC_BAR = (v & 2) != 0;
+                tma<TG, WORLD, MODE, 16, 4>();
+            }
+        MC_AG = MC_BAR = false;
     } else if (WHAT == "ctas") {
         for (int cap : {16, 32, 64, 0}) {
             lsu<TG, WORLD, MODE, S::U, S::THREADS, S::MINB>(cap);
@@ -258,9 +301,81 @@ void dispatch_world() {
     }
 }
 
+// One multicast object over W devices; each device binds `bytes` of its own VMM memory
+// (readable / writable by every device, so unicast peer stores keep working) and maps
+// the object.  Returns per device the local and the multicast VA.
+static void make_multicast(size_t bytes, std::vector<void *> &local, std::vector<void *> &mcva) {
+    CUmulticastObjectProp prop = {};
+    prop.numDevices = W;
+    prop.handleTypes = CU_MEM_HANDLE_TYPE_NONE;
+    prop.size = bytes;
+    size_t gran = 0;
+    CU(cuMulticastGetGranularity(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+    const size_t sz = (bytes + gran - 1) / gran * gran;
+    prop.size = sz;
+    CUmemGenericAllocationHandle mc;
+    CU(cuMulticastCreate(&mc, &prop));
+    for (int d = 0; d < W; ++d) {
+        CUdevice dev;
+        CU(cuDeviceGet(&dev, d));
+        CU(cuMulticastAddDevice(mc, dev));
+    }
+    std::vector<CUmemAccessDesc> acc(W);
+    for (int q = 0; q < W; ++q) {
+        acc[q] = {};
+        acc[q].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        acc[q].location.id = q;
+        acc[q].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    }
+    local.resize(W);
+    mcva.resize(W);
+    for (int d = 0; d < W; ++d) {
+        CK(cudaSetDevice(d));
+        CUmemAllocationProp ap = {};
+        ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        ap.location.id = d;
+        CUmemGenericAllocationHandle ph;
+        CU(cuMemCreate(&ph, sz, &ap, 0));
+        CU(cuMulticastBindMem(mc, 0, ph, 0, sz, 0));
+        CUdeviceptr va = 0, mva = 0;
+        CU(cuMemAddressReserve(&va, sz, 0, 0, 0));
+        CU(cuMemMap(va, sz, 0, ph, 0));
+        CU(cuMemSetAccess(va, sz, acc.data(), W));
+        CU(cuMemAddressReserve(&mva, sz, 0, 0, 0));
+        CU(cuMemMap(mva, sz, 0, mc, 0));
+        CU(cuMemSetAccess(mva, sz, &acc[d], 1));
+        CK(cudaMemset(reinterpret_cast<void *>(va), 0, sz));
+        CK(cudaDeviceSynchronize());
+        local[d] = reinterpret_cast<void *>(va);
+        mcva[d] = reinterpret_cast<void *>(mva);
+    }
+}
+
+static void setup_multicast() {
+    const bool mp = MODE_ == kSgdMp;
+    const size_t bytes = L * (MODE_ == kSgd ? 4 : (mp ? 2 : (DT == GDRAA_BF16 ? 2 : 4)));
+    for (int s = 0; s < 3; ++s) {
+        std::vector<void *> local, mcva;
+        make_multicast(bytes, local, mcva);
+        for (int d = 0; d < W; ++d) {
+            if (MODE_ == kSgd) B[d].w[s] = static_cast<float *>(local[d]);
+            else if (mp) B[d].model[s] = local[d];
+            else B[d].g[s] = local[d];
+            B[d].mc_dst[s] = mcva[d];
+        }
+    }
+    std::vector<void *> local, mcva;
+    make_multicast(64, local, mcva);
+    for (int d = 0; d < W; ++d) {
+        B[d].bar_local = static_cast<uint64_t *>(local[d]);
+        B[d].mc_bar = static_cast<uint64_t *>(mcva[d]);
+    }
+}
+
 int main(int argc, char **argv) {
     if (argc < 5) {
-        std::fprintf(stderr, "usage: tune <world> <L> <f32|bf16> <sgd|mp|mean> [iters] [lib|lsu|tma|tail|ctas|solo]\n");
+        std::fprintf(stderr, "usage: tune <world> <L> <f32|bf16> <sgd|mp|mean> [iters] [lib|lsu|tma|tail|ctas|solo|mc|ve]\n");
         return 1;
     }
     W = std::atoi(argv[1]);
@@ -275,6 +390,8 @@ int main(int argc, char **argv) {
         SOLO = true;
         WHAT = "lib";
     }
+    MC = WHAT == "mc";
+    if (MC) CU(cuInit(0));
     CK(cudaGetDeviceCount(&NDEV));
     if (NDEV < W) {
         std::fprintf(stderr, "need %d GPUs, have %d\n", W, NDEV);
@@ -309,6 +426,7 @@ int main(int argc, char **argv) {
         CK(cudaMemset(tr, 0, 64 * kMaxWorld * 8 * 8));
         TR.push_back(tr);
     }
+    if (MC) setup_multicast();
     void *eh;
     CK(cudaHostAlloc(&eh, sizeof(ErrBlock), cudaHostAllocMapped | cudaHostAllocPortable));
     std::memset(eh, 0, sizeof(ErrBlock));
