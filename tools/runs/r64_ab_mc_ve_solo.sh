@@ -6,6 +6,11 @@ set -x; mkdir -p gpurun_out
 nvidia-smi -L
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/c_build.log 2>&1; echo build=$?
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -I include -o tools/tune tools/tune.cu -lcuda; echo nvcc=$?
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/c_pytest_n4.log 2>&1; echo pytest=$?
+tail -3 gpurun_out/c_pytest_n4.log
+for N in 2 4; do
+  timeout 600 python3 bench.py --gpus $N --config r50bf16mp --e2e-steps 3 --no-nccl > gpurun_out/c_bench_n${N}_r50bf16mp.json 2> gpurun_out/c_bench_n${N}_mp.err; echo benchmp$N=$?
+done
 for rep in 1 2 3; do
   timeout 300 python bench.py --no-cpu-baseline --e2e-steps 3 > gpurun_out/c_ab_now_$rep.json 2> gpurun_out/c_ab_now_$rep.err; echo now=$?
   GDRAA_LIB_PATH=$PWD/paper_1802_02326_b200/lib_ab/libgdraa_b48b841.so timeout 300 python bench.py --no-cpu-baseline --e2e-steps 3 > gpurun_out/c_ab_old_$rep.json 2> gpurun_out/c_ab_old_$rep.err; echo old=$?
