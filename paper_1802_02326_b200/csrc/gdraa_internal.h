@@ -30,6 +30,13 @@ struct alignas(128) Pad {
     uint64_t ll_calls;             // calls served by the small-message (LL) path
     uint64_t mc_calls;             // calls that used the multicast barrier (tools/tune.cu A/B)
     uint64_t _p3[10];
+    // Distributed exit (kFlagDistExit): every CTA of sender p adds the elements it finished
+    // (pulled, folded, pushed) to recv_done[p] of every peer after its fence; the owner's
+    // last CTA waits until recv_done[p] reaches recv_expect[p] + len_p (cumulative).
+    uint64_t recv_done[kMaxWorld];     // written by peers (remote atomics)
+    uint64_t _p4[16 - kMaxWorld];
+    uint64_t recv_expect[kMaxWorld];   // written by the owner's last CTA
+    uint64_t _p5[16 - kMaxWorld];
 };
 static_assert(sizeof(Pad) % 128 == 0, "pad layout");
 
@@ -90,6 +97,9 @@ constexpr uint32_t kFlagCtaFence = 1u;
 // kFlagMcPeersOnly: the mc_dst group holds the N-1 peers only; the own copy is stored
 // locally as well.
 constexpr uint32_t kFlagMcPeersOnly = 2u;
+// kFlagDistExit: the exit synchronisation without the last-CTA relay -- each CTA tells
+// every peer directly how many elements it finished (TMA kernel; GDRAA_DIST_EXIT=1).
+constexpr uint32_t kFlagDistExit = 4u;
 uint32_t env_kernel_flags();
 constexpr int kModes = 3;
 

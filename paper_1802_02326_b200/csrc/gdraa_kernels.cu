@@ -78,6 +78,9 @@ __device__ __forceinline__ void set_half(uint4 &o, int h, uint2 v) {
         o.w = v.y;
     }
 }
+__device__ __forceinline__ void red_add_release_sys(uint64_t *p, uint64_t v) {
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void mc_red_add_release(uint64_t *p, uint64_t v) {
     asm volatile("multimem.red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -997,6 +1000,7 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     auto stage_v = [&](int s) { return stage_w(s) + C::CH; };
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    uint64_t my_elems = 0;   // thread 0: elements of the chunks this CTA claimed (+ tail)
     if (warp == 0) {
         // producer: a3 loads (and the local w, v) of one chunk per stage
         if (lane == 0) {
@@ -1023,6 +1027,7 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
                 uint64_t e0;
                 uint32_t n_el;
                 chunk(c, e0, n_el);
+                my_elems += n_el;
                 mbar_arrive_tx(&full[s], n_el * C::PER_EL);
 #pragma unroll
                 for (int k = 0; k < WORLD; ++k) {
@@ -1169,11 +1174,20 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(2);
     GDRAA_STAMP_DONE();
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const bool cta_fence = (p.flags & kFlagCtaFence) != 0;
+    const bool dist = WORLD > 1 && !mcb && (p.flags & kFlagDistExit) != 0;
+    const bool cta_fence = (p.flags & kFlagCtaFence) != 0 || dist;
     if (WORLD > 1 && !cta_fence) fence_acq_rel_sys();
     __syncthreads();
     if (threadIdx.x == 0) {
         if (WORLD > 1 && cta_fence) fence_acq_rel_sys();
+        if (dist) {
+            if (blockIdx.x == gridDim.x - 1) my_elems += len - lenv;   // the ragged tail
+#pragma unroll 1
+            for (int j = 1; j < WORLD; ++j) {
+                const int q = (rank + j) % WORLD;
+                red_add_release_sys(&p.pad[vr][q]->recv_done[rank], my_elems);
+            }
+        }
         const unsigned prev = atomicAdd(&mine->arrive, 1u);
         s_last = (prev == gridDim.x - 1);
         if (s_last) __threadfence();
@@ -1181,7 +1195,23 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     __syncthreads();
     if (!s_last) return;
     if (threadIdx.x == 0) GDRAA_STAMP(3);
-    if (WORLD > 1 && mcb) {
+    if (dist) {
+        // every CTA of every peer q has finished (its pulls of our g done, its pushes into
+        // our w performed) once recv_done[q] covers q's whole shard
+        if (threadIdx.x < WORLD && threadIdx.x != rank) {
+            const int q = threadIdx.x;
+            const uint64_t oq = min(static_cast<uint64_t>(q) * p.blk, p.n);
+            const uint64_t target = mine->recv_expect[q] + min(p.blk, p.n - oq);
+            if (!wait_geq(&mine->recv_done[q], target, p.timeout_ns, p.abort)) {
+                report_timeout(p.err, 2, q, vr);
+                s_abort = 1;
+            } else {
+                mine->recv_expect[q] = target;
+            }
+        }
+        __syncthreads();
+        if (s_abort) return;
+    } else if (WORLD > 1 && mcb) {
         if (threadIdx.x == 0) {
             mc_red_add_release(p.mc_bar[vr] + 1, 1);
             if (!wait_geq(p.bar_local[vr] + 1, mc_target, p.timeout_ns, p.abort)) {

@@ -15,11 +15,17 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_cuda(), reason="needs 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("kernel", ["lsu", "tma"])
+@pytest.mark.parametrize("kernel", ["lsu", "tma", "tma-dist-exit", "lsu-thread-fence"])
 def test_forced_kernel_parity(kernel):
-    env = dict(os.environ, GDRAA_KERNEL=kernel, GDRAA_LL_MAX_BYTES="0")
+    """Each data-movement variant, and each exit-synchronisation variant (per-thread
+    fence; per-CTA element counts sent to the peers), gives the oracle's bits."""
+    env = dict(os.environ, GDRAA_KERNEL=kernel.split("-")[0], GDRAA_LL_MAX_BYTES="0")
+    if kernel.endswith("dist-exit"):
+        env["GDRAA_DIST_EXIT"] = "1"
+    if kernel.endswith("thread-fence"):
+        env["GDRAA_EXIT_FENCE"] = "thread"
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_kernel_parity_worker.py")],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert f"OK {kernel}" in r.stdout
+    assert f"OK {kernel.split('-')[0]}" in r.stdout
 

@@ -342,6 +342,34 @@ def test_world1_iter_done_flag(world1):
         assert st["iter_done"] == st["calls"] == k + k // 2, st
 
 
+def test_world1_calls_on_alternating_streams(world1):
+    """Calls share the rank's pad (epoch, arrival and work counters): a call issued on
+    another stream than the previous one must not overlap it on the device.  Two buffer
+    sets stepped alternately on two streams with no user synchronisation equal the
+    oracle (without the library's ordering the two grids would share one work counter)."""
+    L = 3_000_017
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    sets = []
+    for k in range(2):
+        gs = make_grads("like", 90 + k, 1, L, False)
+        w0, v0 = synth.w_like(90 + k, L), np.zeros(L, np.float32)
+        g, w, v = to_dev(gs[0]), to_dev(w0), to_dev(v0)
+        gdraa.gdraa_register(w)
+        gdraa.gdraa_register(g)
+        sets.append([gs, w0, v0, g, w, v])
+    torch.cuda.synchronize()
+    for it in range(6):
+        for k, st in enumerate(sets):
+            gs, w0, v0, g, w, v = st
+            gdraa.gdraa_sgd_step(w, g, v, 0.1, 0.9, stream=(s1, s2)[(it + k) % 2])
+            st[1], st[2] = oracle.sgd_step(gs, w0, v0, 0.1, 0.9)
+    torch.cuda.synchronize()
+    for k, (gs, w0, v0, g, w, v) in enumerate(sets):
+        compare(from_dev(w), w0, "f32", what=f"set {k} w")
+        compare(from_dev(v), v0, "f32", what=f"set {k} v")
+    assert gdraa.gdraa_get_stats()["iter_done"] == 12
+
+
 def test_world1_errors(world1):
     a = torch.zeros(1000, device=DEV)
     b = torch.zeros(1000, device=DEV)
@@ -524,3 +552,54 @@ def test_vr_range_rejects_bad_ranges():
         with pytest.raises(gdraa.GdraaError) as e:
             gdraa.gdraa_vr_sgd_step_range(w, g, v, bad[0], bad[1], 0.1, 0.9)
         assert e.value.name == "GDRAA_EINVAL", bad
+
+
+# ---------------------------------------------------------------------------------------
+# Randomised call sequences: every entry point, sizes on both sides of every threshold,
+# chained state, one persistent set of pads / LL slots per world size.
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("N", [3, 8])
+def test_vr_random_call_sequence(N):
+    rng = np.random.default_rng(1000 + N)
+    lim = gdraa.gdraa_small_step_bytes(N) // 4
+    sizes = [1, 7, 64, 1000, lim - 1, lim + 1, 3 * lim + 5, 1_000_003]
+    for step in range(14):
+        L = int(rng.choice(sizes))
+        kind = rng.choice(["mean", "sgd", "ex", "mp", "range"])
+        bf16 = bool(rng.integers(0, 2))
+        gs = make_grads("like", 2000 + 17 * step + N, N, L, bf16)
+        g_d = [to_dev(g, bf16) for g in gs]
+        what = f"step {step} {kind} N={N} L={L} bf16={bf16}"
+        if kind == "mean":
+            gdraa.gdraa_vr_allreduce_mean(g_d)
+            torch.cuda.synchronize()
+            exp = oracle.allreduce_mean(gs)
+            for r in range(N):
+                compare(from_dev(g_d[r]), exp, "bf16" if bf16 else "f32", what=f"{what} r{r}")
+            continue
+        w0, v0 = synth.w_like(3000 + step, L), synth.w_like(4000 + step, L)
+        v_d = [to_dev(v0) for _ in range(N)]
+        if kind == "mp":
+            wm_d = [to_dev(w0) for _ in range(N)]
+            mo_d = [torch.zeros(L, dtype=torch.bfloat16, device=DEV) for _ in range(N)]
+            gdraa.gdraa_vr_sgd_step_mp(wm_d, mo_d, g_d, v_d, 0.1, 0.9, 0.001)
+            we, ve, me = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, 0.001, model_dtype=oracle.BF16)
+            torch.cuda.synchronize()
+            for r in range(N):
+                compare(from_dev(mo_d[r]), me, "bf16", what=f"{what} model r{r}")
+            continue
+        w_d = [to_dev(w0) for _ in range(N)]
+        wd = 0.0 if kind == "sgd" else 0.001
+        if kind == "range" and L >= 16:
+            cut = (L // 2) // 8 * 8
+            for first, count in ((cut, L - cut), (0, cut)):
+                gdraa.gdraa_vr_sgd_step_range(w_d, g_d, v_d, first, count, 0.1, 0.9, wd)
+        elif kind == "sgd":
+            gdraa.gdraa_vr_sgd_step(w_d, g_d, v_d, 0.1, 0.9)
+        else:
+            gdraa.gdraa_vr_sgd_step_ex(w_d, g_d, v_d, 0.1, 0.9, wd)
+        we, ve = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, wd)
+        torch.cuda.synchronize()
+        for r in range(N):
+            compare(from_dev(w_d[r]), we, "f32", what=f"{what} w r{r}")

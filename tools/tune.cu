@@ -384,6 +384,8 @@ int main(int argc, char **argv) {
     MODE_ = std::string(argv[4]) == "mean" ? kMean : (std::string(argv[4]) == "mp" ? kSgdMp : kSgd);
     if (const char *f = std::getenv("GDRAA_EXIT_FENCE"))
         FLAGS = std::strcmp(f, "thread") == 0 ? 0u : kFlagCtaFence;
+    if (const char *f = std::getenv("GDRAA_DIST_EXIT"))
+        if (f[0] == '1') FLAGS |= kFlagDistExit;
     if (argc > 5) ITERS = std::atoi(argv[5]);
     if (argc > 6) WHAT = argv[6];
     if (WHAT == "solo") {
@@ -418,7 +420,8 @@ int main(int argc, char **argv) {
         if (SOLO && d == 0) {   // every peer "has arrived" at every epoch
             Pad h;
             std::memset(&h, 0, sizeof h);
-            for (int q = 0; q < kMaxWorld; ++q) h.entry[q] = h.exit[q] = 1ull << 60;
+            for (int q = 0; q < kMaxWorld; ++q)
+                h.entry[q] = h.exit[q] = h.recv_done[q] = 1ull << 60;
             CK(cudaMemcpy(B[d].pad, &h, sizeof h, cudaMemcpyHostToDevice));
         }
         uint64_t *tr;
