@@ -30,9 +30,9 @@ struct alignas(128) Pad {
     uint64_t ll_calls;             // calls served by the small-message (LL) path
     uint64_t mc_calls;             // calls that used the multicast barrier (tools/tune.cu A/B)
     uint64_t _p3[10];
-    // Distributed exit (kFlagDistExit): every CTA of sender p adds the elements it finished
-    // (pulled, folded, pushed) to recv_done[p] of every peer after its fence; the owner's
-    // last CTA waits until recv_done[p] reaches recv_expect[p] + len_p (cumulative).
+    // Distributed exit (kFlagDistExit, experimental): every CTA of sender p adds the
+    // elements it finished (pulled, folded, pushed) to recv_done[p] of every peer after its
+    // fence; the owner's last CTA waits until recv_done[p] reaches recv_expect[p] + len_p.
     uint64_t recv_done[kMaxWorld];     // written by peers (remote atomics)
     uint64_t _p4[16 - kMaxWorld];
     uint64_t recv_expect[kMaxWorld];   // written by the owner's last CTA
@@ -74,14 +74,16 @@ struct KParams {
     const volatile int32_t *abort;           // host-mapped job-server abort flag, or null:
                                              // spins give up early once a rank has died
     uint32_t flags;                          // kFlag* bits (launch-variant switches)
-    // NVLS multicast variants of the two-shot TMA kernel (set only by
-    // tools/tune.cu for the A/B, null in the library): mc_dst[vr] = multicast VA of the
-    // broadcast buffer (one multimem.st reaches every member of the group); mc_bar[vr] =
-    // multicast VA of a {entry, exit} u64 counter block whose local copy is bar_local[vr]
-    // (one multimem.red per rank and barrier instead of N-1 flag stores).
+#ifdef GDRAA_EXPERIMENTAL
+    // Measured-and-rejected variants of the two-shot TMA kernel, compiled only into
+    // tools/tune.cu for the A/B, never into the library.  NVLS multicast:
+    // mc_dst[vr] = multicast VA of the broadcast buffer (one multimem.st reaches every
+    // member of the group); mc_bar[vr] = multicast VA of a {entry, exit} u64 counter block
+    // whose local copy is bar_local[vr] (one multimem.red per rank and barrier).
     void *mc_dst[kMaxWorld];
     uint64_t *mc_bar[kMaxWorld];
     uint64_t *bar_local[kMaxWorld];
+#endif
 #ifdef GDRAA_TRACE
     uint64_t *trace;                         // tools/tune.cu only: %globaltimer stamps
 #endif
@@ -94,11 +96,11 @@ enum Mode { kMean = 0, kSgd = 1, kSgdMp = 2 };
 // KParams::flags.  kFlagCtaFence: at exit, one fence.acq_rel.sys per CTA after
 // __syncthreads() instead of one per thread (default; GDRAA_EXIT_FENCE=thread clears it).
 constexpr uint32_t kFlagCtaFence = 1u;
-// kFlagMcPeersOnly: the mc_dst group holds the N-1 peers only; the own copy is stored
-// locally as well.
+// Experimental (tools/tune.cu only, GDRAA_EXPERIMENTAL): kFlagMcPeersOnly -- the mc_dst
+// group holds the N-1 peers only, the own copy is stored locally as well; kFlagDistExit
+// -- the exit synchronisation without the last-CTA relay, each CTA telling every peer
+// directly how many elements it finished (measured slower: DESIGN.md §11).
 constexpr uint32_t kFlagMcPeersOnly = 2u;
-// kFlagDistExit: the exit synchronisation without the last-CTA relay -- each CTA tells
-// every peer directly how many elements it finished (TMA kernel; GDRAA_DIST_EXIT=1).
 constexpr uint32_t kFlagDistExit = 4u;
 uint32_t env_kernel_flags();
 constexpr int kModes = 3;

@@ -941,11 +941,16 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP_START();
+#ifdef GDRAA_EXPERIMENTAL
     // multicast barrier variant: counters reach (mc_calls + 1) * N once every rank arrived
     const bool mcb = WORLD > 1 && p.mc_bar[vr] != nullptr;
+#else
+    constexpr bool mcb = false;
+#endif
     const uint64_t mc_target =
         mcb ? (*reinterpret_cast<volatile uint64_t *>(&mine->mc_calls) + 1) * WORLD : 0;
     // a2: "2nd synchronization"
+#ifdef GDRAA_EXPERIMENTAL
     if (WORLD > 1 && mcb) {
         if (blockIdx.x == 0 && threadIdx.x == 0) mc_red_add_release(p.mc_bar[vr], 1);
         __syncthreads();
@@ -953,7 +958,9 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
             report_timeout(p.err, 1, rank, vr);
             s_abort = 1;
         }
-    } else if (WORLD > 1) {
+    } else
+#endif
+    if (WORLD > 1) {
         if (blockIdx.x == 0 && threadIdx.x < WORLD && threadIdx.x != rank)
             st_release_sys(&p.pad[vr][threadIdx.x]->entry[rank], epoch);
         __syncthreads();
@@ -1000,7 +1007,7 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     auto stage_v = [&](int s) { return stage_w(s) + C::CH; };
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    uint64_t my_elems = 0;   // thread 0: elements of the chunks this CTA claimed (+ tail)
+    uint64_t my_elems = 0;   // thread 0: elements of the chunks this CTA claimed (dist exit)
     if (warp == 0) {
         // producer: a3 loads (and the local w, v) of one chunk per stage
         if (lane == 0) {
@@ -1044,7 +1051,11 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     } else {
         // consumers: a4 fold (+ a5 update) from shared memory, a6 push
         const int ct = threadIdx.x - 32;
+#ifdef GDRAA_EXPERIMENTAL
         void *const mcd = WORLD > 1 ? p.mc_dst[vr] : nullptr;   // multicast broadcast (A/B)
+#else
+        void *const mcd = nullptr;
+#endif
         const bool mc_self = (p.flags & kFlagMcPeersOnly) != 0;
         for (uint32_t it = 0;; ++it) {
             const int s = it % C::STAGES;
@@ -1174,12 +1185,17 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     if (blockIdx.x == 0 && threadIdx.x == 0) GDRAA_STAMP(2);
     GDRAA_STAMP_DONE();
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef GDRAA_EXPERIMENTAL
     const bool dist = WORLD > 1 && !mcb && (p.flags & kFlagDistExit) != 0;
+#else
+    constexpr bool dist = false;
+#endif
     const bool cta_fence = (p.flags & kFlagCtaFence) != 0 || dist;
     if (WORLD > 1 && !cta_fence) fence_acq_rel_sys();
     __syncthreads();
     if (threadIdx.x == 0) {
         if (WORLD > 1 && cta_fence) fence_acq_rel_sys();
+#ifdef GDRAA_EXPERIMENTAL
         if (dist) {
             if (blockIdx.x == gridDim.x - 1) my_elems += len - lenv;   // the ragged tail
 #pragma unroll 1
@@ -1188,6 +1204,7 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
                 red_add_release_sys(&p.pad[vr][q]->recv_done[rank], my_elems);
             }
         }
+#endif
         const unsigned prev = atomicAdd(&mine->arrive, 1u);
         s_last = (prev == gridDim.x - 1);
         if (s_last) __threadfence();
@@ -1195,6 +1212,7 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     __syncthreads();
     if (!s_last) return;
     if (threadIdx.x == 0) GDRAA_STAMP(3);
+#ifdef GDRAA_EXPERIMENTAL
     if (dist) {
         // every CTA of every peer q has finished (its pulls of our g done, its pushes into
         // our w performed) once recv_done[q] covers q's whole shard
@@ -1221,7 +1239,9 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
         }
         __syncthreads();
         if (s_abort) return;
-    } else if (WORLD > 1) {
+    } else
+#endif
+    if (WORLD > 1) {
         if (threadIdx.x < WORLD && threadIdx.x != rank)
             st_release_sys(&p.pad[vr][threadIdx.x]->exit[rank], epoch);
         if (threadIdx.x < WORLD && threadIdx.x != rank) {
@@ -1351,10 +1371,14 @@ int env_max_ctas() {
 // sources in flight still fit the 64 registers of two 512-thread CTAs per SM.
 // N = 1 with the dynamic schedule (profiles/r09_tune_n1.jsonl): 2 x 512 threads, U=1 is
 // best (84.1 us = 6081 GB/s vs 88.2 us for 1024 x U=2).
+// N = 1 asks for 3 co-resident 512-thread CTAs per SM (<= 42 registers): without the
+// reciprocal refinement of the division (N = 1 divides by nothing) the compiler otherwise
+// pipelines the loop into 58 registers, 2 CTAs per SM, and the launch runs 2% slower
+// (profiles/r65_n1_ab.json: 80.5 vs 78.8 us at 36 registers).
 template <typename TG, int WORLD, int MODE> struct Shape {
     static constexpr int U = WORLD == 1 ? 1 : (WORLD <= 4 ? 2 : 1);
     static constexpr int THREADS = WORLD == 2 ? 1024 : 512;
-    static constexpr int MINB = WORLD == 2 ? 1 : 2;
+    static constexpr int MINB = WORLD == 1 ? 3 : (WORLD == 2 ? 1 : 2);
 };
 
 using KernelFn = void (*)(KParams);

@@ -415,15 +415,10 @@ struct VrDevice {
 // __syncthreads() (default) -- measured 6-7 us faster per call than one per thread at
 // R50 (N = 2: 166.5 -> 160.0 us, N = 4: 244.1 -> 237.3 us; profiles/r62_fence_ab.json);
 // GDRAA_EXIT_FENCE=thread restores the per-thread fence for A/B runs.
-// GDRAA_DIST_EXIT=1: the exit synchronisation of the TMA kernel as per-CTA element counts
-// sent straight to the peers (kFlagDistExit), for A/B runs.
 uint32_t env_kernel_flags() {
     static const uint32_t v = [] {
         const char *e = std::getenv("GDRAA_EXIT_FENCE");
-        uint32_t f = (e != nullptr && std::strcmp(e, "thread") == 0) ? 0u : kFlagCtaFence;
-        const char *d = std::getenv("GDRAA_DIST_EXIT");
-        if (d != nullptr && d[0] == '1') f |= kFlagDistExit;
-        return f;
+        return (e != nullptr && std::strcmp(e, "thread") == 0) ? 0u : kFlagCtaFence;
     }();
     return v;
 }

@@ -15,13 +15,11 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_cuda(), reason="needs 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("kernel", ["lsu", "tma", "tma-dist-exit", "lsu-thread-fence"])
+@pytest.mark.parametrize("kernel", ["lsu", "tma", "tma-thread-fence", "lsu-thread-fence"])
 def test_forced_kernel_parity(kernel):
-    """Each data-movement variant, and each exit-synchronisation variant (per-thread
-    fence; per-CTA element counts sent to the peers), gives the oracle's bits."""
+    """Each data-movement variant, with the default per-CTA exit fence and with the
+    per-thread one (GDRAA_EXIT_FENCE=thread), gives the oracle's bits."""
     env = dict(os.environ, GDRAA_KERNEL=kernel.split("-")[0], GDRAA_LL_MAX_BYTES="0")
-    if kernel.endswith("dist-exit"):
-        env["GDRAA_DIST_EXIT"] = "1"
     if kernel.endswith("thread-fence"):
         env["GDRAA_EXIT_FENCE"] = "thread"
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_kernel_parity_worker.py")],

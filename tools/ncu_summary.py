@@ -3,7 +3,7 @@
 and the key counters of one `--set full` capture.
 
     python tools/ncu_summary.py launches <launches.csv>            > profiles/…_launches.json
-    python tools/ncu_summary.py full <prof.ncu-rep> [algorithmic_bytes] > profiles/…_ncu.json
+    python tools/ncu_summary.py full <prof.ncu-rep | raw.csv> [algorithmic_bytes] > profiles/…_ncu.json
 """
 import csv
 import io
@@ -48,8 +48,13 @@ def launches(path):
 
 
 def full(path, algorithmic=None):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    """path: an .ncu-rep, or the CSV of `ncu -i <rep> --page raw --csv` (reduced on the
+    GPU box to keep gpurun_out small)."""
+    if path.endswith(".csv"):
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, units = rows[0], rows[1]
     res = []

@@ -16,6 +16,7 @@
 //     solo: the library shapes with rank 0 alone (barriers pre-satisfied): one rank's
 //           NVLink traffic in one direction pair, and a kernel ncu can replay
 #define GDRAA_TRACE 1
+#define GDRAA_EXPERIMENTAL 1   // the measured-and-rejected variants (multicast, dist exit)
 #include "../paper_1802_02326_b200/csrc/gdraa_kernels.cu"
 
 #include <cuda.h>
@@ -239,6 +240,8 @@ void sweep() {
         tma<TG, WORLD, MODE, 16, 4>();
     } else if (WHAT == "lsu") {
         lsu<TG, WORLD, MODE, 1, 512, 2>();
+        lsu<TG, WORLD, MODE, 1, 512, 3>();
+        lsu<TG, WORLD, MODE, 1, 512, 4>();
         lsu<TG, WORLD, MODE, 2, 512, 2>();
         lsu<TG, WORLD, MODE, 2, 1024, 1>();
         lsu<TG, WORLD, MODE, 4, 512, 1>();
