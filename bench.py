@@ -614,7 +614,15 @@ def main():
             roof["hbm_side"] = {"bytes_per_launch": hb,
                                 "achieved_gbs": hb / (ms_step * 1e-3) / 1e9,
                                 "frac_of_peak": hb / (ms_step * 1e-3) / 1e9 / peaks["hbm_gbs"]}
-        roof["traffic"] = ncu_traffic(args.config, N)
+        tr = ncu_traffic(args.config, N)
+        if isinstance(tr, dict):   # N >= 2: the solo rank-0 capture
+            roof["traffic"] = tr["dram_bytes"]
+            roof["traffic_nvlink"] = {k: tr[k] for k in (
+                "kind", "nvlink_rx_user_bytes", "nvlink_tx_user_bytes", "nvlink_rx_bytes",
+                "nvlink_tx_bytes", "algorithmic_nvlink_bytes_own_share_per_direction",
+                "nvlink_user_over_algorithmic", "source") if k in tr}
+        else:
+            roof["traffic"] = tr
         roof["kernel_ms"] = ms_step
         cpu = None
         if N == 1 and not args.no_cpu_baseline:
