@@ -51,7 +51,19 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-// NVLS multicast (the address is a multicast VA: the switch delivers to every member).
+// The h-th 8-byte half of a bf16 output vector (4 or 8 values).
+__device__ __forceinline__ void set_half(uint2 &o, int, uint2 v) { o = v; }
+__device__ __forceinline__ void set_half(uint4 &o, int h, uint2 v) {
+    if (h == 0) {
+        o.x = v.x;
+        o.y = v.y;
+    } else {
+        o.z = v.x;
+        o.w = v.y;
+    }
+}
+// NVLS multicast stores (the address is a multicast VA: the switch delivers to every
+// member); reached only from the experimental multicast branch (mc_dst != null).
 __device__ __forceinline__ void mc_st(uint4 *p, uint4 v) {
     asm volatile("multimem.st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(__uint_as_float(v.x)),
                  "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
@@ -67,23 +79,14 @@ __device__ __forceinline__ void mc_st_bf16(uint4 *p, uint4 v) {
                  "r"(v.z), "r"(v.w)
                  : "memory");
 }
-// The h-th 8-byte half of a bf16 output vector (4 or 8 values).
-__device__ __forceinline__ void set_half(uint2 &o, int, uint2 v) { o = v; }
-__device__ __forceinline__ void set_half(uint4 &o, int h, uint2 v) {
-    if (h == 0) {
-        o.x = v.x;
-        o.y = v.y;
-    } else {
-        o.z = v.x;
-        o.w = v.y;
-    }
-}
+#ifdef GDRAA_EXPERIMENTAL   // tools/tune.cu only
 __device__ __forceinline__ void red_add_release_sys(uint64_t *p, uint64_t v) {
     asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void mc_red_add_release(uint64_t *p, uint64_t v) {
     asm volatile("multimem.red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+#endif
 __device__ __forceinline__ void fence_acq_rel_sys() {
     asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
@@ -944,11 +947,11 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
 #ifdef GDRAA_EXPERIMENTAL
     // multicast barrier variant: counters reach (mc_calls + 1) * N once every rank arrived
     const bool mcb = WORLD > 1 && p.mc_bar[vr] != nullptr;
+    const uint64_t mc_target =
+        mcb ? (*reinterpret_cast<volatile uint64_t *>(&mine->mc_calls) + 1) * WORLD : 0;
 #else
     constexpr bool mcb = false;
 #endif
-    const uint64_t mc_target =
-        mcb ? (*reinterpret_cast<volatile uint64_t *>(&mine->mc_calls) + 1) * WORLD : 0;
     // a2: "2nd synchronization"
 #ifdef GDRAA_EXPERIMENTAL
     if (WORLD > 1 && mcb) {
@@ -1371,14 +1374,20 @@ int env_max_ctas() {
 // sources in flight still fit the 64 registers of two 512-thread CTAs per SM.
 // N = 1 with the dynamic schedule (profiles/r09_tune_n1.jsonl): 2 x 512 threads, U=1 is
 // best (84.1 us = 6081 GB/s vs 88.2 us for 1024 x U=2).
-// N = 1 asks for 3 co-resident 512-thread CTAs per SM (<= 42 registers): without the
-// reciprocal refinement of the division (N = 1 divides by nothing) the compiler otherwise
-// pipelines the loop into 58 registers, 2 CTAs per SM, and the launch runs 2% slower
-// (profiles/r65_n1_ab.json: 80.5 vs 78.8 us at 36 registers).
+// N = 1 (the local fused SGD): once the division by N = 1 compiles to nothing, the
+// round-1 shape (U1 x 512 x 2/SM) pipelines into 58 registers and 2 CTAs per SM, 2%
+// slower than at 36 registers (profiles/r65_ab_mc_ve_dist.json); re-swept
+// (profiles/r66_tune_n1_lsu.jsonl, tools/tune lsu): U4 x 512 x 1/SM is the fastest.
+// GDRAA_N1_U / _THREADS / _MINB override it at compile time (A/B builds only).
+#ifndef GDRAA_N1_U
+#define GDRAA_N1_U 4
+#define GDRAA_N1_THREADS 512
+#define GDRAA_N1_MINB 1
+#endif
 template <typename TG, int WORLD, int MODE> struct Shape {
-    static constexpr int U = WORLD == 1 ? 1 : (WORLD <= 4 ? 2 : 1);
-    static constexpr int THREADS = WORLD == 2 ? 1024 : 512;
-    static constexpr int MINB = WORLD == 1 ? 3 : (WORLD == 2 ? 1 : 2);
+    static constexpr int U = WORLD == 1 ? GDRAA_N1_U : (WORLD <= 4 ? 2 : 1);
+    static constexpr int THREADS = WORLD == 1 ? GDRAA_N1_THREADS : (WORLD == 2 ? 1024 : 512);
+    static constexpr int MINB = WORLD == 1 ? GDRAA_N1_MINB : (WORLD == 2 ? 1 : 2);
 };
 
 using KernelFn = void (*)(KParams);
@@ -1564,20 +1573,23 @@ cudaError_t launch_gdraa_ll_sgd(const KParams &p, int dtype, int mode, int vr_ro
     return launch_pdl(fn, grid, block, s, p);
 }
 
-// Which data-movement variant serves a call (both produce the same bits).  Measured with
-// bench.py at R50/R101 (profiles/r23_bench_kernel_choice.json): the TMA-staged kernel
-// is 1.2-2.5% faster for fp32 gradients at N >= 2 and for bf16 at N = 4, 1-2.6% slower
-// for bf16 at N <= 2 and equal at N = 1.  GDRAA_KERNEL=lsu|tma forces one.
+// Which data-movement variant serves a call (both produce the same bits): the TMA-staged
+// kernel at every N >= 2.  Round 1 kept the LSU kernel for bf16 at N <= 2 (1-2.6% faster
+// then, profiles/r23_bench_kernel_choice.json); with the per-CTA exit fence the TMA kernel
+// wins every bf16 mode at N = 2 and 4 as well (profiles/r66_tune_choice.jsonl: sgd
+// 123.5 vs 124.9 us, mean 87.9 vs 89.3, _mp 88.8 vs 90.7 at N = 2; 182.7 vs 188.1, 128.0
+// vs 132.9, 128.9 vs 133.6 at N = 4).  N = 1 has no peers: the LSU kernel.
+// GDRAA_KERNEL=lsu|tma forces one.
 bool use_tma_kernel(int dtype, int mode, int world) {
     static const int forced = [] {
         const char *e = std::getenv("GDRAA_KERNEL");
         if (e == nullptr) return -1;
         return std::string(e) == "tma" ? 1 : (std::string(e) == "lsu" ? 0 : -1);
     }();
+    (void)dtype;
+    (void)mode;
     if (forced >= 0) return forced == 1;
-    if (world < 2) return false;
-    if (dtype == GDRAA_F32) return true;
-    return world >= 4 && mode != kMean;
+    return world >= 2;
 }
 
 cudaError_t launch_gdraa_tma(const KParams &p, int dtype, int mode, int vr_rows,
