@@ -429,3 +429,75 @@ def test_multiprocess_full_size_sampled(tmp_path):
         js.communicate(timeout=120)
     for r in range(world):
         assert json.load(open(tmp_path / f"full{r}.json"))["checked"] > 0
+
+
+# ---------------------------------------------------------------------------------------
+# World 8 on fewer GPUs (opt-in): two or more ranks per GPU, each its own process and CUDA
+# context, time-sliced by the GPU.  Slow, but it runs the whole N = 8 multi-process path
+# -- job server with 8 ranks, 7 IPC peers per registration (same-GPU and cross-GPU),
+# 8-way barriers, the LL slots at N = 8 -- on a 2- or 4-GPU box.
+# ---------------------------------------------------------------------------------------
+
+def _over_worker(rank, world, ndev, sock, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    import synth
+    from paper_1802_02326_b200 import gdraa
+    from tests._parity import compare
+    from tests.test_gpu_parity import from_dev, make_grads, to_dev
+
+    d = rank % ndev
+    torch.cuda.set_device(d)
+    dev = f"cuda:{d}"
+    os.environ["GDRAA_JOBSERVER"] = sock
+    gdraa.gdraa_init(world, rank)
+    calls = 0
+    for L in (1000, 70_001, 1 << 20, 3_000_017):       # LL and two-shot paths at N = 8
+        for bf16 in (False, True):
+            gs = make_grads("like", 81 + L % 89, world, L, bf16)
+            dt = "bf16" if bf16 else "f32"
+            buf = to_dev(gs[rank], bf16, dev)
+            gdraa.gdraa_register(buf)
+            gdraa.gdraa_allreduce_mean(buf)
+            calls += 1
+            torch.cuda.synchronize()
+            compare(from_dev(buf), oracle.allreduce_mean(gs), dt, what=f"w8 mean L={L} r{rank}")
+            w0, v0 = synth.w_like(82, L), synth.w_like(83, L)
+            g = to_dev(gs[rank], bf16, dev)
+            w, v = to_dev(w0, dev=dev), to_dev(v0, dev=dev)
+            gdraa.gdraa_register(w)
+            gdraa.gdraa_register(g)
+            off, ln = gdraa.gdraa_shard(world, rank, L)
+            for it in range(2):
+                w0, v0 = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, 0.001)
+                gdraa.gdraa_sgd_step_ex(w, g, v, 0.1, 0.9, 0.001)
+                calls += 1
+            torch.cuda.synchronize()
+            compare(from_dev(w), w0, "f32", what=f"w8 sgd w L={L} {dt} r{rank}")
+            compare(from_dev(v)[off:off + ln], v0[off:off + ln], "f32", what=f"w8 v r{rank}")
+            for t in (buf, w, g):
+                gdraa.gdraa_deregister(t)
+    st = gdraa.gdraa_get_stats()
+    assert st["calls"] == calls and st["iter_done"] == calls, (st, calls)
+    gdraa.gdraa_finalize()
+    with open(os.path.join(out_dir, f"w8_{rank}.json"), "w") as f:
+        json.dump({"calls": calls, "device": d, "stats": st}, f)
+
+
+@pytest.mark.skipif(os.environ.get("GDRAA_TEST_OVERSUBSCRIBE") != "1",
+                    reason="opt-in (GDRAA_TEST_OVERSUBSCRIBE=1): world 8, several ranks per GPU")
+def test_multiprocess_world8_oversubscribed(tmp_path):
+    from paper_1802_02326_b200 import jobserver
+    world, ndev = 8, torch.cuda.device_count()
+    sock = str(tmp_path / "js.sock")
+    js = jobserver.start(world, sock)
+    try:
+        mp.start_processes(_over_worker, args=(world, ndev, sock, str(tmp_path)), nprocs=world,
+                           join=True, start_method="spawn")
+    finally:
+        out, err = js.communicate(timeout=300)
+    line = json.loads(out.strip().splitlines()[-1])["jobserver"]
+    reps = [json.load(open(tmp_path / f"w8_{r}.json")) for r in range(world)]
+    assert line["ok"] and line["data_bytes"] == 0 and line["ranks_joined"] == 8, line
+    assert line["done"] == [reps[0]["calls"]] * world, line
