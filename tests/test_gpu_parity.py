@@ -603,3 +603,55 @@ def test_vr_random_call_sequence(N):
         torch.cuda.synchronize()
         for r in range(N):
             compare(from_dev(w_d[r]), we, "f32", what=f"{what} w r{r}")
+
+
+# ---------------------------------------------------------------------------------------
+# Maximum sizes: a buffer past 2^32 bytes (64-bit indexing of elements, chunks and byte
+# offsets), inputs built on the device from an integer formula the host can recompute on
+# any window, compared with the oracle on windows at the start, at every 2^31- and
+# 2^32-byte boundary, at the shard boundary and at the ragged end.
+# ---------------------------------------------------------------------------------------
+
+def _int_formula(i, p, lo, span, salt):
+    """Integer values in [lo, lo + span) from index i (int64 array / tensor) and rank p,
+    exactly representable in fp32 (|value| < 2^24); identical on host and device."""
+    return ((i * 2654435761 + (p + 1) * 40503 + salt) >> 7) % span + lo
+
+
+def _fill_device(L, p, lo, span, salt, dev=DEV, chunk=1 << 26):
+    out = torch.empty(L, dtype=torch.float32, device=dev)
+    for a in range(0, L, chunk):
+        i = torch.arange(a, min(L, a + chunk), dtype=torch.int64, device=dev)
+        out[a:a + i.numel()] = _int_formula(i, p, lo, span, salt).to(torch.float32)
+    return out
+
+
+def test_vr_max_size_64bit_indexing():
+    N = 2
+    L = (1 << 30) + 9                       # 4 GiB + 36 B of fp32 per buffer
+    free, _ = torch.cuda.mem_get_info()
+    if free < 3 * N * L * 4 + (4 << 30):
+        pytest.skip("not enough device memory")
+    # integer family (exact for N a power of two): g in [-2^13, 2^13), w in [-2^12, 2^12),
+    # v in [-2^10, 2^10), lr = 2^-3, mom = 2^-1
+    g_d = [_fill_device(L, p, -(1 << 13), 1 << 14, 11) for p in range(N)]
+    w_d = [_fill_device(L, 0, -(1 << 12), 1 << 13, 22) for _ in range(N)]
+    v_d = [_fill_device(L, 0, -(1 << 10), 1 << 11, 33) for _ in range(N)]
+    gdraa.gdraa_vr_sgd_step(w_d, g_d, v_d, synth.INT_LR, synth.INT_MOM)
+    torch.cuda.synchronize()
+    off1, _ = gdraa.gdraa_shard(N, 1, L)
+    W = 4096
+    starts = sorted({0, (1 << 29) - W // 2, (1 << 30) - W, off1 - W // 2, L - W,
+                     (1 << 28) - W // 2, 3 * (1 << 28) - W // 2})
+    for a in starts:
+        i = np.arange(a, a + W, dtype=np.int64)
+        gs = [_int_formula(i, p, -(1 << 13), 1 << 14, 11).astype(np.float32) for p in range(N)]
+        w0 = _int_formula(i, 0, -(1 << 12), 1 << 13, 22).astype(np.float32)
+        v0 = _int_formula(i, 0, -(1 << 10), 1 << 11, 33).astype(np.float32)
+        we, ve = oracle.sgd_step(gs, w0, v0, synth.INT_LR, synth.INT_MOM)
+        for r in range(N):
+            compare(from_dev(w_d[r][a:a + W]), we, "f32", what=f"max-size w @{a} r{r}")
+            off, ln = gdraa.gdraa_shard(N, r, L)
+            lo, hi = max(a, off), min(a + W, off + ln)
+            if lo < hi:
+                compare(from_dev(v_d[r][lo:hi]), ve[lo - a:hi - a], "f32", what=f"v @{a} r{r}")
