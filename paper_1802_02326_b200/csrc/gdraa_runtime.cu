@@ -126,6 +126,17 @@ struct Registration {
     void *peer[kMaxWorld] = {};
 };
 
+// Calls share their pad (epoch, arrival and work counters) and LL slots, so a call issued
+// on another stream than the previous one first waits for everything issued so far on the
+// previous call's stream (an event recorded there at that moment; calls on one stream pay
+// nothing, and programmatic dependent launch between them is kept).  Not while either
+// stream is capturing: a graph's own edges order the calls captured into it.
+struct StreamOrder {
+    cudaStream_t last = nullptr;
+    cudaEvent_t ev = nullptr;
+    bool have = false;
+};
+
 struct State {
     bool inited = false;
     int world = 0, rank = 0, device = 0;
@@ -148,15 +159,8 @@ struct State {
     uint64_t timeout_ns = 30000000000ull;
     bool gated = false;
     uint64_t issued = 0;
-    // Cross-stream ordering: every call shares this rank's pad (epoch, arrival and work
-    // counters) and LL slots, so a call issued on another stream than the previous one
-    // first waits for everything issued so far on the previous call's stream (an event
-    // recorded there at that moment; calls on one stream pay nothing, and programmatic
-    // dependent launch between them is kept).  Not while either stream is capturing:
-    // a graph's own edges order the calls captured into it.
-    cudaStream_t last_stream = nullptr;
-    cudaEvent_t order_ev = nullptr;
-    bool have_last = false;
+    // Cross-stream ordering (see StreamOrder): every call shares this rank's pad and LL slots.
+    StreamOrder order;
     bool fatal = false;
     int fatal_code = 0;
     std::string fatal_msg;
@@ -348,7 +352,12 @@ void fill_common(KParams &p, uint64_t n) {
     p.ll_sleep_ns = static_cast<uint32_t>(env_u64("GDRAA_LL_SLEEP_NS", 256));
     p.flags = env_kernel_flags();
     p.err = g.err_d;
-    p.done[0] = g.done_d;
+    // GDRAA_NO_DONE=1 (A/B only): skip the IterDone store into the host-mapped page
+    static const bool no_done = [] {
+        const char *e = std::getenv("GDRAA_NO_DONE");
+        return e != nullptr && e[0] == '1';
+    }();
+    p.done[0] = no_done ? nullptr : g.done_d;
     p.abort = g.abort_d;
 }
 
@@ -372,20 +381,18 @@ bool capturing(cudaStream_t s) {
 }
 
 // Before a launch on s: order it after the previous call if that was on another stream.
-int order_after_previous(cudaStream_t s) {
-    if (!g.have_last || s == g.last_stream || capturing(s) || capturing(g.last_stream))
-        return GDRAA_OK;
-    if (g.order_ev == nullptr)
-        CUDA_TRY(cudaEventCreateWithFlags(&g.order_ev, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventRecord(g.order_ev, g.last_stream));
-    CUDA_TRY(cudaStreamWaitEvent(s, g.order_ev, 0));
+int order_after_previous(StreamOrder &o, cudaStream_t s) {
+    if (!o.have || s == o.last || capturing(s) || capturing(o.last)) return GDRAA_OK;
+    if (o.ev == nullptr) CUDA_TRY(cudaEventCreateWithFlags(&o.ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(o.ev, o.last));
+    CUDA_TRY(cudaStreamWaitEvent(s, o.ev, 0));
     return GDRAA_OK;
 }
 
 // After a launch on s: remember the stream.
-int note_launch(cudaStream_t s) {
-    g.last_stream = s;
-    g.have_last = true;
+int note_launch(StreamOrder &o, cudaStream_t s) {
+    o.last = s;
+    o.have = true;
     return GDRAA_OK;
 }
 
@@ -407,6 +414,7 @@ struct VrDevice {
     uint4 *ll[kMaxWorld + 1] = {};      // ll[world] -> `world` LL receive areas
     uint64_t ll_pairs[kMaxWorld + 1] = {};
     ErrBlock *err_h = nullptr, *err_d = nullptr;
+    StreamOrder order;                  // virtual-rank calls share these pads too
 };
 
 }  // namespace
@@ -547,23 +555,25 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
     p.ll_sleep_ns = static_cast<uint32_t>(env_u64("GDRAA_LL_SLEEP_NS", 256));
     p.flags = env_kernel_flags();
     const size_t es = dtype == GDRAA_F32 ? 4 : 2;
+    rc = order_after_previous(d->order, s);
+    if (rc) return rc;
     if (mode == kMean && world > 1 && n * es <= 8 * p.ll_pairs) {   // latency path
         cudaError_t e = launch_gdraa_ll(p, dtype, world, true, s);
         if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr LL launch: %s", cudaGetErrorString(e));
-        return GDRAA_OK;
+        return note_launch(d->order, s);
     }
     if (upd && world > 1 && n * es <= ll_sgd_limit_bytes(world) &&
         ll_sgd_fits(p.blk, dtype, mode, p.ll_pairs)) {   // small-message SGD step
         cudaError_t e = launch_gdraa_ll_sgd(p, dtype, mode, world, true, s);
         if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr LL SGD launch: %s", cudaGetErrorString(e));
-        return GDRAA_OK;
+        return note_launch(d->order, s);
     }
     int gx = 0;
     cudaError_t e = use_tma_kernel(dtype, mode, world)
                         ? launch_gdraa_tma(p, dtype, mode, world, true, s, &gx)
                                      : launch_gdraa(p, dtype, mode, world, true, s, &gx);
     if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr kernel launch: %s", cudaGetErrorString(e));
-    return GDRAA_OK;
+    return note_launch(d->order, s);
 }
 
 }  // namespace
@@ -621,7 +631,7 @@ static void release_resources() {
     if (g.page_registered) cudaHostUnregister(g.page);
     if (g.page) munmap(g.page, 4096);
     if (g.err_h) cudaFreeHost(g.err_h);
-    if (g.order_ev) cudaEventDestroy(g.order_ev);
+    if (g.order.ev) cudaEventDestroy(g.order.ev);
     State s;
     g = s;
 }
@@ -838,7 +848,7 @@ static int mean_common(void *buf, size_t first, size_t count, gdraa_stream_t s) 
         p.dst[0][q] = offset_ptr(r->peer[q], first, es);
     }
     const cudaStream_t cs = reinterpret_cast<cudaStream_t>(s);
-    rc = order_after_previous(cs);
+    rc = order_after_previous(g.order, cs);
     if (rc) return rc;
     if (g.ll != nullptr && count * es <= 8 * g.ll_pairs) {
         // small message: the latency path (same result, bit for bit)
@@ -850,7 +860,7 @@ static int mean_common(void *buf, size_t first, size_t count, gdraa_stream_t s) 
         if (rc) return rc;
     }
     account(count, r->dtype, 0);
-    return note_launch(cs);
+    return note_launch(g.order, cs);
 }
 
 int gdraa_allreduce_mean(void *buf, gdraa_stream_t s) { return mean_common(buf, 0, SIZE_MAX, s); }
@@ -902,7 +912,7 @@ static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, 
     p.v[0] = static_cast<float *>(offset_ptr(v, first, 4));
     p.wm[0] = mode == kSgdMp ? static_cast<float *>(offset_ptr(wm, first, 4)) : nullptr;
     const cudaStream_t cs = reinterpret_cast<cudaStream_t>(s);
-    rc = order_after_previous(cs);
+    rc = order_after_previous(g.order, cs);
     if (rc) return rc;
     if (g.ll != nullptr && count * eg <= g.ll_sgd_limit &&
         ll_sgd_fits(p.blk, rg->dtype, mode, g.ll_pairs)) {
@@ -915,7 +925,7 @@ static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, 
         if (rc) return rc;
     }
     account(count, rg->dtype, mode == kSgd ? 4 : 2);
-    return note_launch(cs);
+    return note_launch(g.order, cs);
 }
 
 int gdraa_sgd_step(float *w, const void *gr, float *v, float lr, float mom, gdraa_stream_t s) {
