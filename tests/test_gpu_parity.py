@@ -655,3 +655,26 @@ def test_vr_max_size_64bit_indexing():
             lo, hi = max(a, off), min(a + W, off + ln)
             if lo < hi:
                 compare(from_dev(v_d[r][lo:hi]), ve[lo - a:hi - a], "f32", what=f"v @{a} r{r}")
+
+
+def test_vr_calls_on_alternating_streams():
+    """Virtual-rank calls share one set of pads per world size: calls alternating between
+    two streams without user synchronisation must still run one after the other."""
+    N, L = 4, 2_000_003
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    sets = []
+    for k in range(2):
+        gs = make_grads("like", 95 + k, N, L, False)
+        w0, v0 = synth.w_like(95 + k, L), np.zeros(L, np.float32)
+        sets.append([gs, w0, v0, [to_dev(g) for g in gs], [to_dev(w0) for _ in range(N)],
+                     [to_dev(v0) for _ in range(N)]])
+    torch.cuda.synchronize()
+    for it in range(4):
+        for k, st in enumerate(sets):
+            gs, w0, v0, g_d, w_d, v_d = st
+            gdraa.gdraa_vr_sgd_step(w_d, g_d, v_d, 0.1, 0.9, stream=(s1, s2)[(it + k) % 2])
+            st[1], st[2] = oracle.sgd_step(gs, w0, v0, 0.1, 0.9)
+    torch.cuda.synchronize()
+    for k, (gs, w0, v0, g_d, w_d, v_d) in enumerate(sets):
+        for r in range(N):
+            compare(from_dev(w_d[r]), w0, "f32", what=f"set {k} w r{r}")
