@@ -352,12 +352,9 @@ void fill_common(KParams &p, uint64_t n) {
     p.ll_sleep_ns = static_cast<uint32_t>(env_u64("GDRAA_LL_SLEEP_NS", 256));
     p.flags = env_kernel_flags();
     p.err = g.err_d;
-    // GDRAA_NO_DONE=1 (A/B only): skip the IterDone store into the host-mapped page
-    static const bool no_done = [] {
-        const char *e = std::getenv("GDRAA_NO_DONE");
-        return e != nullptr && e[0] == '1';
-    }();
-    p.done[0] = no_done ? nullptr : g.done_d;
+    // IterDone: the last CTA's store into the host-mapped page costs nothing measurable
+    // (profiles/r69_alpha.json: two-shot sgd sweep with and without it within 0.2 us)
+    p.done[0] = g.done_d;
     p.abort = g.abort_d;
 }
 
