@@ -415,8 +415,7 @@ def main():
     # SGD, small steps take the LL kernel (no device barrier), the rest the two-shot one
     code = gdraa.GDRAA_BF16 if g_dt == "bf16" else gdraa.GDRAA_F32
     path = ("local" if N == 1 else
-            "ll_sgd" if L * s_g <= gdraa.gdraa_small_step_bytes(N, code, mp) else
-            "rb" if L * s_g <= gdraa.gdraa_rb_message_bytes(N) else "two_shot")
+            "ll_sgd" if L * s_g <= gdraa.gdraa_small_step_bytes(N, code, mp) else "two_shot")
 
     def barrier():
         if world > 1:

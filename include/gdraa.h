@@ -74,16 +74,12 @@ typedef enum {
  * Uses the CUDA device current on the calling thread.  For world > 1 the job server
  * socket path is read from the environment variable GDRAA_JOBSERVER (started by
  * paper_1802_02326_b200.jobserver); the call blocks until all ranks have joined and the
- * signal pads are mapped (GDRAA_CONNECT_TIMEOUT_MS, default 120000).  The path
- * thresholds (GDRAA_LL_MAX_BYTES, GDRAA_LL_SGD_MAX_BYTES, GDRAA_RB_MAX_BYTES) are read
- * here, fixed for the communicator's lifetime and checked to agree on every rank, since
- * they decide which kernel -- with which synchronisation protocol -- serves a call; so
- * are the SM count and GDRAA_MAX_CTAS, which fix the receive-buffer kernel's grid (its
- * CTA b pairs with CTA b of every peer).  Device memory owned by the library per rank:
- * the signal pad, the small-message slots (2 x world x 2 x GDRAA_LL_MAX_BYTES) and the
- * receive buffer (2 x GDRAA_RB_MAX_BYTES + 64 KiB of flags).
+ * signal pads are mapped (GDRAA_CONNECT_TIMEOUT_MS, default 120000).  The small-message
+ * thresholds (GDRAA_LL_MAX_BYTES, GDRAA_LL_SGD_MAX_BYTES) are read here, fixed for the
+ * communicator's lifetime and checked to agree on every rank, since they decide which
+ * kernel -- with which synchronisation protocol -- serves a call.
  * Errors: EINVAL (range), ESTATE (already initialised), ESHAPE (ranks disagree on the
- * thresholds or the grid), EJOBSERVER, ECUDA.  A failed call releases whatever it had acquired
+ * thresholds), EJOBSERVER, ECUDA.  A failed call releases whatever it had acquired
  * (pads, mappings, socket), so it may be retried.
  */
 int gdraa_init(int world, int rank);
@@ -230,20 +226,6 @@ size_t gdraa_small_message_bytes(int world);
  * (gdraa_small_message_bytes) can hold.  Pure host function (reads the environment).
  */
 size_t gdraa_small_step_bytes(int world, int dtype, int mixed);
-
-/*
- * gdraa_rb_message_bytes -- the largest payload (n * sizeof(g) or of buf, bytes per rank)
- * that the collective calls above the small-message limits serve with the receive-buffer
- * kernel: the paper's own push design (Fig. 3), every rank writing block D(r, q)
- * into owner q's receive buffer RB and the owner writing its averaged / updated block back
- * into every rank; CTA b of every rank handles the same chunks, so both synchronisations
- * are per-CTA-pair flags that travel behind the data instead of device-wide
- * barriers.  Larger calls take the two-shot pull kernel.  Results are bitwise those of
- * every other path.  Default 64 MiB (GDRAA_RB_MAX_BYTES overrides, 0 disables; read at
- * gdraa_init and checked to agree across ranks); the receive area is twice that per rank.
- * Returns 0 for world < 2 or out of range.  Pure host function (reads the environment).
- */
-size_t gdraa_rb_message_bytes(int world);
 
 typedef struct {
     uint64_t calls;            /* collective calls completed on the device (device counter) */

@@ -74,12 +74,6 @@ struct KParams {
     const volatile int32_t *abort;           // host-mapped job-server abort flag, or null:
                                              // spins give up early once a rank has died
     uint32_t flags;                          // kFlag* bits (launch-variant switches)
-    // Receive-buffer ("RB") path, the paper's push design: rank q's RB area seen
-    // from vr -- kRbFlagBytes of flags [2 phases][kMaxWorld senders][kRbMaxCtas] u64, then
-    // the data slots [2 parities][world senders][rb_cap bytes].
-    char *rb[kMaxWorld][kMaxWorld];
-    uint64_t rb_cap;                         // bytes per sender slot (>= blk * sizeof(g))
-    uint32_t rb_chunk;                       // elements per chunk (multiple of 64)
 #ifdef GDRAA_EXPERIMENTAL
     // Measured-and-rejected variants of the two-shot TMA kernel, compiled only into
     // tools/tune.cu for the A/B, never into the library.  NVLS multicast:
@@ -116,9 +110,6 @@ constexpr int kModes = 3;
 cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows,
                          bool cooperative, cudaStream_t s, int *grid_x_out);
 
-// GDRAA_MAX_CTAS (0: no cap), read once per process.
-int env_max_ctas();
-
 // Max co-resident CTAs of the kernel for (dtype, mode, world) on this device.
 int max_ctas(int dtype, int mode, int world);
 
@@ -149,25 +140,6 @@ uint64_t ll_sgd_limit_bytes(int world);
 // (profiles/r15_sweep*_ll*.jsonl), i.e. ~4 MiB / (N-1) as the LL bytes grow with N-1.
 // GDRAA_LL_MAX_BYTES overrides it (0 disables the LL path).
 uint64_t ll_limit_bytes(int world);
-
-// Receive-buffer path (gdraa_rb_kernel): every rank pushes block D(r, q) of its gradient
-// into owner q's receive slot, the owner folds and updates its shard and pushes w' to every
-// rank; CTA b of every rank handles the same chunks (c = b mod G), so the two
-// synchronisations become per-CTA-pair flags and no device-wide barrier runs.
-constexpr int kRbMaxCtas = 512;
-constexpr uint64_t kRbFlagBytes = 2ull * kMaxWorld * kRbMaxCtas * 8;
-constexpr uint32_t kRbChunk = 2048;
-constexpr uint64_t kRbBaseBytes = 64ull << 20;
-// Largest gradient payload (n * sizeof(g), bytes per rank) served by the RB path and the
-// size of the receive slots (GDRAA_RB_MAX_BYTES overrides, 0 disables); per-sender slot
-// bytes and total RB area bytes for a world size.
-uint64_t rb_limit_bytes(int world);
-uint64_t rb_cap_bytes(int world);
-inline uint64_t rb_area_bytes(int world, uint64_t cap) { return kRbFlagBytes + 2ull * world * cap; }
-cudaError_t launch_gdraa_rb(const KParams &p, int dtype, int mode, int vr_rows, bool cooperative,
-                            cudaStream_t s);
-// Grid of the RB kernel for a shard of blk elements (the same on every rank).
-int rb_grid(uint64_t blk, int vr_rows);
 constexpr uint64_t kLLBaseBytes = 4ull << 20;
 constexpr uint64_t kLLSgdBaseBytes = 4ull << 20;
 

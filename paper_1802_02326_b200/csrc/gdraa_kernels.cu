@@ -1268,229 +1268,6 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
     }
 }
 
-// ---------------------------------------------------------------------------------
-// Receive-buffer ("RB") kernel: Algorithm 1 in the paper's own data flow (blocks
-// are written into the receiver's buffer RB, the averaged block is written back), for
-// messages between the small-message limit and rb_limit_bytes.  Every rank:
-//   1  "Reduce" (push): copies block D(rank, q) of its g into owner q's receive slot
-//      [par][rank] for every q != rank, then flags it (Fig. 3a);
-//   2  "Aggregation" + update: once every sender's block of its shard has arrived, folds
-//      own g and the N-1 received blocks in ascending rank, divides once, applies the
-//      momentum step, and pushes w' (or the mean) into every rank (Fig. 3b), then flags it;
-//   3  waits until every peer's w' has arrived (the paper's 1st synchronisation).
-// CTA b of every rank handles the same chunks c = b, b + G, ... of every shard (the grid
-// G is the same on every rank), so each synchronisation is a flag from CTA b of the peer
-// to CTA b here: flags[phase][sender][b] = epoch.  No device-wide barrier, no last-CTA
-// relay; the arrival of a CTA pair's data is that pair's synchronisation (the two
-// synchronisations per call of P:119, split over the CTA pairs).
-// Hazards: RAW on the received blocks and on w' -- the flags (release / acquire); WAR on a
-// peer's w against its forward -- w' for shard r is pushed only after every rank's block
-// of shard r arrived, i.e. after every rank entered the call; WAR on a receive slot --
-// slots alternate by epoch parity, and a sender at call e has received every rank's w'
-// of call e-1, sent after that rank consumed its slot of call e-1 (slot e-2's parity was
-// consumed before that).  g is never read by another rank.
-// ---------------------------------------------------------------------------------
-__device__ __forceinline__ uint4 ld_cg(const uint4 *p) {
-    uint4 r;
-    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-__device__ __forceinline__ uint2 ld_cg(const uint2 *p) {
-    uint2 r;
-    asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-    return r;
-}
-
-template <typename TG, int WORLD, int MODE>
-__global__ void __launch_bounds__(512, 1)
-gdraa_rb_kernel(const __grid_constant__ KParams p) {
-    using EL = Elem<TG>;
-    using Raw = typename EL::Raw;
-    constexpr bool kUpdate = MODE != kMean;
-    constexpr int T = 512;                   // one 4-element vector per thread and chunk
-    static_assert(kRbChunk == T * E, "RB chunk = one vector per thread");
-    const int vr = blockIdx.y;
-    const int rank = p.rank0 + vr;
-    const int b = blockIdx.x;
-    const int G = gridDim.x;
-    Pad *mine = p.pad[vr][rank];
-    __shared__ int s_abort, s_last;
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint64_t epoch = *reinterpret_cast<volatile uint64_t *>(&mine->epoch) + 1;
-    const uint64_t par = epoch & 1u;
-    if (threadIdx.x == 0) s_abort = 0;
-    constexpr uint64_t CH = kRbChunk;
-    auto shard = [&](int q, uint64_t &o, uint64_t &l) {
-        o = min(static_cast<uint64_t>(q) * p.blk, p.n);
-        l = min(p.blk, p.n - o);
-    };
-    // flags of rank q's area: [phase][sender][cta]
-    auto flag = [&](int q, int phase, int sender) {
-        return reinterpret_cast<uint64_t *>(p.rb[vr][q]) +
-               (static_cast<uint64_t>(phase) * kMaxWorld + sender) * kRbMaxCtas + b;
-    };
-    // rank q's receive slot for `sender` (this call's parity)
-    auto slot = [&](int q, int sender) {
-        return reinterpret_cast<TG *>(p.rb[vr][q] + kRbFlagBytes +
-                                      (par * WORLD + sender) * p.rb_cap);
-    };
-    const TG *const gl = static_cast<const TG *>(p.src[vr][rank]);
-
-    // 1: push my blocks D(rank, q) into every owner's slot [par][rank]
-#pragma unroll 1
-    for (int j = 1; j < WORLD; ++j) {
-        const int q = (rank + j) % WORLD;
-        uint64_t oq, lq;
-        shard(q, oq, lq);
-        const uint64_t nvec = lq / E;
-        const Raw *from = reinterpret_cast<const Raw *>(gl + oq);
-        Raw *to = reinterpret_cast<Raw *>(slot(q, rank));
-        // chunk c = vectors [c*T, (c+1)*T): one vector per thread; 4 of this CTA's chunks
-        // in flight per pass
-        for (uint64_t c0 = b; c0 * T < nvec; c0 += 4ull * G) {
-            Raw v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint64_t k = (c0 + u * G) * T + threadIdx.x;
-                if (k < nvec) v[u] = ld_stream(from + k);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint64_t k = (c0 + u * G) * T + threadIdx.x;
-                if (k < nvec) st_vec(to + k, v[u]);
-            }
-        }
-        // ragged end (lq % 4 elements) of the last shard: chunk (nvec*E) / CH owns it
-        if (lq % E != 0 && static_cast<int>((nvec * E / CH) % G) == b)
-            for (uint64_t t = nvec * E + threadIdx.x; t < lq; t += T)
-                reinterpret_cast<TG *>(slot(q, rank))[t] = gl[oq + t];
-    }
-    __syncthreads();
-    if (threadIdx.x < WORLD && threadIdx.x != rank)   // release: our pushes, then the flag
-        st_release_sys(flag(threadIdx.x, 0, rank), epoch);
-
-    // 2: my shard -- wait for every sender's blocks of my chunks, fold, update, push w'
-    uint64_t off, len;
-    shard(rank, off, len);
-    if (threadIdx.x < WORLD && threadIdx.x != rank) {
-        if (!wait_geq(flag(rank, 0, threadIdx.x), epoch, p.timeout_ns, p.abort)) {
-            report_timeout(p.err, 1, threadIdx.x, vr);
-            s_abort = 1;
-        }
-    }
-    __syncthreads();
-    if (s_abort) return;
-    const float lr = p.lr, mom = p.mom, wd = p.wd;
-    float *const vloc = p.v[vr];
-    float *const wloc = MODE == kSgdMp ? p.wm[vr] : static_cast<float *>(p.dst[vr][rank]);
-    const Raw *rx[WORLD];
-#pragma unroll
-    for (int q = 0; q < WORLD; ++q)
-        rx[q] = q == rank ? reinterpret_cast<const Raw *>(gl + off)
-                          : reinterpret_cast<const Raw *>(slot(rank, q));
-    const uint64_t nvec = len / E;
-    for (uint64_t c = b; c * T < nvec; c += G) {
-        {
-            const uint64_t k = c * T + threadIdx.x;
-            if (k >= nvec) continue;
-            float x[WORLD][E];
-#pragma unroll
-            for (int q = 0; q < WORLD; ++q)
-                EL::widen(q == rank ? ld_stream(rx[q] + k) : ld_cg(rx[q] + k), x[q]);
-            float m[E];
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                float col[WORLD];
-#pragma unroll
-                for (int q = 0; q < WORLD; ++q) col[q] = x[q][e];
-                m[e] = average<WORLD>(col);
-            }
-            const uint64_t e0 = off + k * E;
-            if (kUpdate) {
-                float4 w = ld_f4(wloc + e0), v = ld_f4(vloc + e0);
-                sgd(m[0], lr, mom, wd, w.x, v.x);
-                sgd(m[1], lr, mom, wd, w.y, v.y);
-                sgd(m[2], lr, mom, wd, w.z, v.z);
-                sgd(m[3], lr, mom, wd, w.w, v.w);
-                st_vec(reinterpret_cast<uint4 *>(vloc + e0), as_u4(v.x, v.y, v.z, v.w));
-                if (MODE == kSgd) {
-                    const uint4 o = as_u4(w.x, w.y, w.z, w.w);
-#pragma unroll
-                    for (int j = 1; j <= WORLD; ++j)
-                        st_vec(reinterpret_cast<uint4 *>(static_cast<float *>(p.dst[vr][(rank + j) % WORLD]) + e0), o);
-                } else {
-                    st_vec(reinterpret_cast<uint4 *>(wloc + e0), as_u4(w.x, w.y, w.z, w.w));
-                    const float wf[E] = {w.x, w.y, w.z, w.w};
-                    const uint2 o = Elem<__nv_bfloat16>::narrow(wf);
-#pragma unroll
-                    for (int j = 1; j <= WORLD; ++j)
-                        st_vec(reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(p.dst[vr][(rank + j) % WORLD]) + e0), o);
-                }
-            } else {
-                const Raw o = EL::narrow(m);
-#pragma unroll
-                for (int j = 1; j <= WORLD; ++j)
-                    st_vec(reinterpret_cast<Raw *>(static_cast<TG *>(p.dst[vr][(rank + j) % WORLD]) + e0), o);
-            }
-        }
-    }
-    // ragged end of the last shard, scalar, by the CTA owning its chunk
-    if (len % E != 0 && static_cast<int>((nvec * E / CH) % G) == b) {
-        for (uint64_t t = nvec * E + threadIdx.x; t < len; t += T) {
-            float col[WORLD];
-#pragma unroll
-            for (int q = 0; q < WORLD; ++q)
-                col[q] = q == rank ? EL::load1(gl, off + t) : EL::load1(slot(rank, q), t);
-            const float m = average<WORLD>(col);
-            const uint64_t e = off + t;
-            if (kUpdate) {
-                float w = wloc[e], v = vloc[e];
-                sgd(m, lr, mom, wd, w, v);
-                vloc[e] = v;
-                if (MODE == kSgd) {
-                    for (int j = 1; j <= WORLD; ++j)
-                        static_cast<float *>(p.dst[vr][(rank + j) % WORLD])[e] = w;
-                } else {
-                    wloc[e] = w;
-                    for (int j = 1; j <= WORLD; ++j)
-                        Elem<__nv_bfloat16>::store1(p.dst[vr][(rank + j) % WORLD], e, w);
-                }
-            } else {
-                for (int j = 1; j <= WORLD; ++j) EL::store1(p.dst[vr][(rank + j) % WORLD], e, m);
-            }
-        }
-    }
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x < WORLD && threadIdx.x != rank)   // release: our w' pushes, then the flag
-        st_release_sys(flag(threadIdx.x, 1, rank), epoch);
-
-    // 3: every peer's w' for my chunks has arrived (peer CTA b pushed chunks c = b mod G)
-    if (threadIdx.x < WORLD && threadIdx.x != rank) {
-        if (!wait_geq(flag(rank, 1, threadIdx.x), epoch, p.timeout_ns, p.abort)) {
-            report_timeout(p.err, 2, threadIdx.x, vr);
-            s_abort = 1;
-        }
-    }
-    __syncthreads();
-    if (s_abort) return;
-    if (threadIdx.x == 0) {
-        const unsigned prev = atomicAdd(&mine->arrive, 1u);
-        s_last = (prev == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (s_last && threadIdx.x == 0) {
-        __threadfence();
-        mine->arrive = 0;
-        mine->calls += 1;
-        if (WORLD > 1) mine->sync_waits += 2;
-        mine->epoch = epoch;
-        if (p.done[vr] != nullptr) *p.done[vr] = epoch;
-    }
-}
-
 using KernelFnLL = void (*)(KParams);
 
 // Programmatic stream serialization hides the launch gap between back-to-back
@@ -1578,6 +1355,13 @@ bool grid_by_small_chunks() {
     return v;
 }
 
+int env_max_ctas() {
+    static const int v = [] {
+        const char *e = std::getenv("GDRAA_MAX_CTAS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
 
 // ---------------------------------------------------------------------------------
 // Launch shapes (measured on B200): vectors in flight per
@@ -1650,14 +1434,6 @@ Launch pick(int dtype, int mode, int world) {
 }
 
 }  // namespace
-
-int env_max_ctas() {
-    static const int v = [] {
-        const char *e = std::getenv("GDRAA_MAX_CTAS");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
 
 int max_ctas(int dtype, int mode, int world) {
     Launch l = pick(dtype, mode, world);
@@ -1875,66 +1651,6 @@ cudaError_t launch_gdraa_tma(const KParams &p, int dtype, int mode, int vr_rows,
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, l.fn, p);
-}
-
-namespace {
-template <typename TG, int MODE>
-KernelFnLL pick_rb_m(int world) {
-    switch (world) {
-        case 2: return gdraa_rb_kernel<TG, 2, MODE>;
-        case 3: return gdraa_rb_kernel<TG, 3, MODE>;
-        case 4: return gdraa_rb_kernel<TG, 4, MODE>;
-        case 5: return gdraa_rb_kernel<TG, 5, MODE>;
-        case 6: return gdraa_rb_kernel<TG, 6, MODE>;
-        case 7: return gdraa_rb_kernel<TG, 7, MODE>;
-        case 8: return gdraa_rb_kernel<TG, 8, MODE>;
-        default: return nullptr;
-    }
-}
-template <typename TG>
-KernelFnLL pick_rb_t(int mode, int world) {
-    switch (mode) {
-        case kMean: return pick_rb_m<TG, kMean>(world);
-        case kSgd: return pick_rb_m<TG, kSgd>(world);
-        case kSgdMp: return pick_rb_m<TG, kSgdMp>(world);
-        default: return nullptr;
-    }
-}
-}  // namespace
-
-// One CTA per SM at most, and no more CTAs than chunks of a shard (every CTA must have
-// work for the flags to pair up cheaply), capped by GDRAA_MAX_CTAS; the same on every rank
-// (SM count, chunk size and the cap are checked to agree at init).
-int rb_grid(uint64_t blk, int vr_rows) {
-    int dev = 0, sms = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-        return 0;
-    uint64_t cap = static_cast<uint64_t>(sms) / vr_rows;
-    const int env_cap = env_max_ctas();
-    if (env_cap > 0 && static_cast<uint64_t>(env_cap) < cap) cap = env_cap;
-    if (cap > static_cast<uint64_t>(kRbMaxCtas)) cap = kRbMaxCtas;
-    const uint64_t chunks = (blk + kRbChunk - 1) / kRbChunk;
-    uint64_t gx = chunks < cap ? chunks : cap;
-    return gx < 1 ? 1 : static_cast<int>(gx);
-}
-
-cudaError_t launch_gdraa_rb(const KParams &p, int dtype, int mode, int vr_rows, bool cooperative,
-                            cudaStream_t s) {
-    KernelFnLL fn = dtype == GDRAA_F32 ? pick_rb_t<float>(mode, p.world)
-                                       : pick_rb_t<__nv_bfloat16>(mode, p.world);
-    if (fn == nullptr) return cudaErrorInvalidValue;
-    const uint64_t es = dtype == GDRAA_F32 ? 4 : 2;
-    if (p.blk * es > p.rb_cap || p.rb_chunk != kRbChunk) return cudaErrorInvalidValue;
-    const int gx = rb_grid(p.blk, vr_rows);
-    if (gx < 1) return cudaErrorInvalidConfiguration;
-    dim3 grid(static_cast<unsigned>(gx), vr_rows), block(512);
-    if (cooperative) {
-        void *args[] = {const_cast<KParams *>(&p)};
-        return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(fn), grid, block, args,
-                                           0, s);
-    }
-    return launch_pdl(fn, grid, block, s, p);
 }
 
 }  // namespace gdraa

@@ -148,9 +148,6 @@ struct State {
     Pad *peer_pad[kMaxWorld] = {};
     uint4 *ll = nullptr;                // small-message receive slots (world > 1)
     uint4 *peer_ll[kMaxWorld] = {};
-    char *rb = nullptr;                 // receive-buffer area (world > 1): flags + slots
-    char *peer_rb[kMaxWorld] = {};
-    uint64_t rb_cap = 0, rb_limit = 0;  // bytes per sender slot; largest RB payload
     uint64_t ll_pairs = 0;
     uint64_t ll_sgd_limit = 0;          // small-message SGD threshold (bytes), fixed at init
     ErrBlock *err_h = nullptr, *err_d = nullptr;
@@ -354,9 +351,6 @@ void fill_common(KParams &p, uint64_t n) {
     p.ll_pairs = g.ll_pairs;
     p.ll_sleep_ns = static_cast<uint32_t>(env_u64("GDRAA_LL_SLEEP_NS", 256));
     p.flags = env_kernel_flags();
-    for (int q = 0; q < g.world; ++q) p.rb[0][q] = g.peer_rb[q];
-    p.rb_cap = g.rb_cap;
-    p.rb_chunk = kRbChunk;
     p.err = g.err_d;
     // IterDone: the last CTA's store into the host-mapped page costs nothing measurable
     // (profiles/r69_alpha.json: two-shot sgd sweep with and without it within 0.2 us)
@@ -416,8 +410,6 @@ struct VrDevice {
     Pad *pads[kMaxWorld + 1] = {};      // pads[world] -> `world` consecutive Pads
     uint4 *ll[kMaxWorld + 1] = {};      // ll[world] -> `world` LL receive areas
     uint64_t ll_pairs[kMaxWorld + 1] = {};
-    char *rb[kMaxWorld + 1] = {};       // rb[world] -> `world` receive-buffer areas
-    uint64_t rb_cap[kMaxWorld + 1] = {};
     ErrBlock *err_h = nullptr, *err_d = nullptr;
     StreamOrder order;                  // virtual-rank calls share these pads too
 };
@@ -440,22 +432,6 @@ uint64_t ll_limit_bytes(int world) {
     if (world < 2) return 0;
     const uint64_t dflt = kLLBaseBytes / static_cast<uint64_t>(world - 1);
     return env_u64("GDRAA_LL_MAX_BYTES", dflt) / 8 * 8;
-}
-
-// Receive-buffer path: up to GDRAA_RB_MAX_BYTES of gradient per rank (default 64 MiB;
-// 0 disables), receive slots sized for it (each sender's block of the largest such call).
-uint64_t rb_limit_bytes(int world) {
-    if (world < 2) return 0;
-    return env_u64("GDRAA_RB_MAX_BYTES", kRbBaseBytes) / 256 * 256;
-}
-
-uint64_t rb_cap_bytes(int world) {
-    const uint64_t lim = rb_limit_bytes(world);
-    if (lim == 0) return 0;
-    // blk of the largest n (bf16: lim / 2 elements) at 4 bytes per element, 256-aligned
-    const uint64_t n = lim / 2, c = (n + world - 1) / world;
-    const uint64_t blk = (c + kQuantum - 1) / kQuantum * kQuantum;
-    return (blk * 4 + 255) / 256 * 256;
 }
 
 uint64_t ll_sgd_limit_bytes(int world) {
@@ -503,16 +479,6 @@ int vr_prepare(int world, VrDevice **out) {
         CUDA_TRY(cudaMemset(lp, 0, ll_area_bytes(world, pairs) * world));
         d.ll[world] = static_cast<uint4 *>(lp);
         d.ll_pairs[world] = pairs;
-    }
-    const uint64_t cap = rb_cap_bytes(world);
-    if (world > 1 && cap > 0 && d.rb[world] == nullptr) {
-        void *rp = nullptr;
-        const size_t one = rb_area_bytes(world, cap);
-        CUDA_TRY(cudaMalloc(&rp, one * world));
-        for (int q = 0; q < world; ++q)
-            CUDA_TRY(cudaMemset(static_cast<char *>(rp) + q * one, 0, kRbFlagBytes));
-        d.rb[world] = static_cast<char *>(rp);
-        d.rb_cap[world] = cap;
     }
     *out = &d;
     return GDRAA_OK;
@@ -577,8 +543,6 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
             if (d->ll[world] != nullptr)
                 p.ll[r][q] = d->ll[world] +
                              q * (ll_area_bytes(world, d->ll_pairs[world]) / sizeof(uint4));
-            if (d->rb[world] != nullptr)
-                p.rb[r][q] = d->rb[world] + q * rb_area_bytes(world, d->rb_cap[world]);
         }
         p.v[r] = upd ? a.v[r] : nullptr;
         p.wm[r] = mode == kSgdMp ? a.wm[r] : nullptr;
@@ -587,8 +551,6 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
     p.ll_pairs = d->ll[world] != nullptr ? d->ll_pairs[world] : 0;
     p.ll_sleep_ns = static_cast<uint32_t>(env_u64("GDRAA_LL_SLEEP_NS", 256));
     p.flags = env_kernel_flags();
-    p.rb_cap = d->rb[world] != nullptr ? d->rb_cap[world] : 0;
-    p.rb_chunk = kRbChunk;
     const size_t es = dtype == GDRAA_F32 ? 4 : 2;
     rc = order_after_previous(d->order, s);
     if (rc) return rc;
@@ -601,12 +563,6 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
         ll_sgd_fits(p.blk, dtype, mode, p.ll_pairs)) {   // small-message SGD step
         cudaError_t e = launch_gdraa_ll_sgd(p, dtype, mode, world, true, s);
         if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr LL SGD launch: %s", cudaGetErrorString(e));
-        return note_launch(d->order, s);
-    }
-    if (world > 1 && d->rb[world] != nullptr && n * es <= rb_limit_bytes(world) &&
-        p.blk * es <= p.rb_cap) {   // mid-size: the receive-buffer path
-        cudaError_t e = launch_gdraa_rb(p, dtype, mode, world, true, s);
-        if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr RB launch: %s", cudaGetErrorString(e));
         return note_launch(d->order, s);
     }
     int gx = 0;
@@ -650,11 +606,6 @@ size_t gdraa_small_step_bytes(int world, int dtype, int mixed) {
     return static_cast<size_t>(n * es);
 }
 
-size_t gdraa_rb_message_bytes(int world) {
-    if (world < 2 || world > kMaxWorld) return 0;
-    return static_cast<size_t>(rb_limit_bytes(world));
-}
-
 int gdraa_shard(int world, int rank, size_t n, size_t *off, size_t *len) {
     if (off == nullptr || len == nullptr) return fail(GDRAA_EINVAL, "null output pointer");
     if (n == 0) return fail(GDRAA_EINVAL, "n must be >= 1");
@@ -674,7 +625,6 @@ static void release_resources() {
     for (auto &kv : g.opened) cudaIpcCloseMemHandle(kv.second);
     if (g.pad) cudaFree(g.pad);
     if (g.ll) cudaFree(g.ll);
-    if (g.rb) cudaFree(g.rb);
     if (g.page_registered) cudaHostUnregister(g.page);
     if (g.page) munmap(g.page, 4096);
     if (g.err_h) cudaFreeHost(g.err_h);
@@ -797,25 +747,9 @@ static int init_impl(int world, int rank) {
         if (rc) return cleanup_fail(rc);
         for (int p = 0; p < world; ++p) g.peer_ll[p] = static_cast<uint4 *>(lpeers[p]);
     }
-    // Receive-buffer area (registration sequence 3): flags + [2][world][rb_cap] bytes.
-    g.rb_limit = rb_limit_bytes(world);
-    g.rb_cap = rb_cap_bytes(world);
-    if (world > 1 && g.rb_limit > 0) {
-        const size_t sz = rb_area_bytes(world, g.rb_cap);
-        void *rp = nullptr;
-        CUDA_TRY(cudaMalloc(&rp, sz));
-        CUDA_TRY(cudaMemset(rp, 0, kRbFlagBytes));
-        CUDA_TRY(cudaDeviceSynchronize());
-        g.rb = static_cast<char *>(rp);
-        void *rpeers[kMaxWorld] = {};
-        int rc = ipc_exchange(g.rb, sz, sz, -3, 4, rpeers);
-        if (rc) return cleanup_fail(rc);
-        for (int p = 0; p < world; ++p) g.peer_rb[p] = static_cast<char *>(rpeers[p]);
-    }
     // Path selection must agree on every rank (a rank on the LL path and a peer on the
-    // two-shot path would wait for each other until the timeout), and so must the RB
-    // kernel's grid (CTA b pairs with CTA b): the thresholds, the SM count and the CTA cap
-    // are fixed here and checked across ranks through the job server (sequence 4).
+    // two-shot path would wait for each other until the timeout): the thresholds are fixed
+    // here and checked across ranks through the job server (registration sequence 3).
     g.ll_sgd_limit = g.ll_pairs ? ll_sgd_limit_bytes(world) : 0;
     if (world > 1) {
         proto::Reg cfg{};
@@ -825,22 +759,10 @@ static int init_impl(int world, int rank) {
         proto::RegOk all{};
         int rc = exchange(cfg, &all);
         if (rc == GDRAA_ESHAPE)
-            rc = fail(GDRAA_ESHAPE, "ranks disagree on the path thresholds or the grid "
-                      "(GDRAA_LL_MAX_BYTES / GDRAA_LL_SGD_MAX_BYTES / GDRAA_RB_MAX_BYTES / "
-                      "GDRAA_MAX_CTAS and the GPU model must match on every rank): %s",
+            rc = fail(GDRAA_ESHAPE, "ranks disagree on the small-message thresholds "
+                      "(GDRAA_LL_MAX_BYTES / GDRAA_LL_SGD_MAX_BYTES must match on every "
+                      "rank): %s",
                       t_err.c_str());
-        if (rc) return cleanup_fail(rc);
-        // the RB kernel's CTA pairing: RB threshold, SM count and CTA cap (sequence 5)
-        int sms = 0;
-        CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g.device));
-        proto::Reg grid{};
-        grid.what = 5;
-        grid.n = g.rb_limit;
-        grid.dtype = static_cast<int32_t>((sms & 0x7FFF) << 16 | std::min(env_max_ctas(), 0xFFFF));
-        rc = exchange(grid, &all);
-        if (rc == GDRAA_ESHAPE)
-            rc = fail(GDRAA_ESHAPE, "ranks disagree on GDRAA_RB_MAX_BYTES, GDRAA_MAX_CTAS or the "
-                      "SM count: %s", t_err.c_str());
         if (rc) return cleanup_fail(rc);
     }
     g.inited = true;
@@ -930,11 +852,6 @@ static int mean_common(void *buf, size_t first, size_t count, gdraa_stream_t s) 
         cudaError_t e = launch_gdraa_ll(p, r->dtype, 1, false, cs);
         if (e != cudaSuccess) return fail(GDRAA_ECUDA, "LL kernel launch: %s", cudaGetErrorString(e));
         g.issued += 1;
-    } else if (g.rb != nullptr && count * es <= g.rb_limit && p.blk * es <= g.rb_cap) {
-        // mid-size: the receive-buffer path (same result, bit for bit)
-        cudaError_t e = launch_gdraa_rb(p, r->dtype, kMean, 1, false, cs);
-        if (e != cudaSuccess) return fail(GDRAA_ECUDA, "RB kernel launch: %s", cudaGetErrorString(e));
-        g.issued += 1;
     } else {
         rc = launch(p, r->dtype, kMean, cs);
         if (rc) return rc;
@@ -999,11 +916,6 @@ static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, 
         // small message: the data carries both synchronisations (same result, bit for bit)
         cudaError_t e = launch_gdraa_ll_sgd(p, rg->dtype, mode, 1, false, cs);
         if (e != cudaSuccess) return fail(GDRAA_ECUDA, "LL SGD kernel launch: %s", cudaGetErrorString(e));
-        g.issued += 1;
-    } else if (g.rb != nullptr && count * eg <= g.rb_limit && p.blk * eg <= g.rb_cap) {
-        // mid-size: the receive-buffer path (same result, bit for bit)
-        cudaError_t e = launch_gdraa_rb(p, rg->dtype, mode, 1, false, cs);
-        if (e != cudaSuccess) return fail(GDRAA_ECUDA, "RB kernel launch: %s", cudaGetErrorString(e));
         g.issued += 1;
     } else {
         rc = launch(p, rg->dtype, mode, cs);

@@ -29,7 +29,7 @@ EXPORTED = ["gdraa_sgd_step_ex", "gdraa_sgd_step_mp", "gdraa_poly_lr",
             "gdraa_shard", "gdraa_get_stats", "gdraa_finalize", "gdraa_last_error",
             "gdraa_version", "gdraa_vr_allreduce_mean", "gdraa_vr_sgd_step",
             "gdraa_vr_allreduce_mean_range", "gdraa_vr_sgd_step_range",
-            "gdraa_vr_sgd_step_mp_range", "gdraa_rb_message_bytes"]
+            "gdraa_vr_sgd_step_mp_range"]
 
 
 class GdraaError(RuntimeError):
@@ -72,7 +72,6 @@ _sig = {
     "gdraa_poly_lr": ([_f, ctypes.c_uint64, ctypes.c_uint64, _f], _f),
     "gdraa_small_message_bytes": ([_i], _sz),
     "gdraa_small_step_bytes": ([_i, _i, _i], _sz),
-    "gdraa_rb_message_bytes": ([_i], _sz),
     "gdraa_allreduce_mean_range": ([_vp, _sz, _sz, _vp], _i),
     "gdraa_sgd_step_range": ([_vp, _vp, _vp, _sz, _sz, _f, _f, _f, _vp], _i),
     "gdraa_sgd_step_mp_range": ([_vp, _vp, _vp, _vp, _sz, _sz, _f, _f, _f, _vp], _i),
@@ -203,10 +202,6 @@ def gdraa_small_message_bytes(world: int) -> int:
 
 def gdraa_small_step_bytes(world: int, dtype: int = GDRAA_F32, mixed: bool = False) -> int:
     return int(_lib.gdraa_small_step_bytes(world, dtype, 1 if mixed else 0))
-
-
-def gdraa_rb_message_bytes(world: int) -> int:
-    return int(_lib.gdraa_rb_message_bytes(world))
 
 
 def gdraa_shard(world: int, rank: int, n: int):

@@ -678,56 +678,3 @@ def test_vr_calls_on_alternating_streams():
     for k, (gs, w0, v0, g_d, w_d, v_d) in enumerate(sets):
         for r in range(N):
             compare(from_dev(w_d[r]), w0, "f32", what=f"set {k} w r{r}")
-
-
-# ---------------------------------------------------------------------------------------
-# The receive-buffer (RB) kernel: sizes between the small-message limits and
-# gdraa_rb_message_bytes, every mode, chained calls (slot parity), ragged ends, grids of
-# fewer CTAs than chunks and of one CTA, interleaved with the other two kernels.
-# ---------------------------------------------------------------------------------------
-
-@pytest.mark.parametrize("N", [2, 3, 4, 8])
-@pytest.mark.parametrize("dt", ["f32", "bf16"])
-def test_vr_rb_path(N, dt):
-    bf16 = dt == "bf16"
-    es = 2 if bf16 else 4
-    code = gdraa.GDRAA_BF16 if bf16 else gdraa.GDRAA_F32
-    rb = gdraa.gdraa_rb_message_bytes(N) // es
-    ll_step = gdraa.gdraa_small_step_bytes(N, code) // es
-    ll_mean = gdraa.gdraa_small_message_bytes(N) // es
-    assert rb > max(ll_step, ll_mean)
-    sizes = [max(ll_step, ll_mean) + 1, max(ll_step, ll_mean) + 4097, 3_000_017, rb - 1, rb]
-    for L in sizes:
-        gs0 = make_grads("like", 1100 + L % 71, N, L, bf16)
-        w, v = synth.w_like(1101, L), synth.w_like(1102, L)
-        w_d = [to_dev(w) for _ in range(N)]
-        v_d = [to_dev(v) for _ in range(N)]
-        for it in range(3):                       # slot parity alternates
-            gs = gs0 if it == 0 else make_grads("like", 1110 + it, N, L, bf16)
-            g_d = [to_dev(g, bf16) for g in gs]
-            w, v = oracle.sgd_step_wd(gs, w, v, synth.PAPER_LR, synth.PAPER_MOM, 0.001)
-            gdraa.gdraa_vr_sgd_step_ex(w_d, g_d, v_d, synth.PAPER_LR, synth.PAPER_MOM, 0.001)
-            torch.cuda.synchronize()
-            for r in range(N):
-                off, ln = gdraa.gdraa_shard(N, r, L)
-                what = f"RB sgd N={N} {dt} L={L} it{it} r{r}"
-                compare(from_dev(w_d[r]), w, "f32", what=what + " w")
-                compare(from_dev(v_d[r])[off:off + ln], v[off:off + ln], "f32", what=what + " v")
-                assert np.array_equal(from_dev(g_d[r]), gs[r]), what + " g changed"
-        # in-place mean and the mixed-precision step on the same size
-        bufs = [to_dev(g, bf16) for g in gs0]
-        gdraa.gdraa_vr_allreduce_mean(bufs)
-        w0, v0 = synth.w_like(1103, L), synth.w_like(1104, L)
-        wm_d = [to_dev(w0) for _ in range(N)]
-        vm_d = [to_dev(v0) for _ in range(N)]
-        mo_d = [torch.zeros(L, dtype=torch.bfloat16, device=DEV) for _ in range(N)]
-        g_d = [to_dev(g, bf16) for g in gs0]
-        gdraa.gdraa_vr_sgd_step_mp(wm_d, mo_d, g_d, vm_d, 0.1, 0.9, 0.001)
-        torch.cuda.synchronize()
-        mean = oracle.allreduce_mean(gs0)
-        we, ve, me = oracle.sgd_step_wd(gs0, w0, v0, 0.1, 0.9, 0.001, model_dtype=oracle.BF16)
-        for r in range(N):
-            compare(from_dev(bufs[r]), mean, dt, what=f"RB mean N={N} L={L} r{r}")
-            compare(from_dev(mo_d[r]), me, "bf16", what=f"RB mp model N={N} L={L} r{r}")
-            off, ln = gdraa.gdraa_shard(N, r, L)
-            compare(from_dev(wm_d[r])[off:off + ln], we[off:off + ln], "f32", what="RB mp master")

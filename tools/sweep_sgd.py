@@ -3,7 +3,6 @@
 fused kernel, fp32 (or bf16) gradients of 1 KiB - 64 MiB per rank.
 
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/sweep_sgd.py --path ll [--graph]
-    torchrun ... tools/sweep_sgd.py --path rb [--graph]        # receive-buffer kernel (<= its limit)
     torchrun ... tools/sweep_sgd.py --path two_shot [--graph]
 
 The path is fixed at gdraa_init from GDRAA_LL_SGD_MAX_BYTES (huge: the LL kernel wherever
@@ -26,11 +25,9 @@ def main():
     ap.add_argument("--max-log2", type=int, default=26)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays")
-    ap.add_argument("--path", default="ll", choices=["ll", "rb", "two_shot"])
+    ap.add_argument("--path", default="ll", choices=["ll", "two_shot"])
     args = ap.parse_args()
     os.environ["GDRAA_LL_SGD_MAX_BYTES"] = str(1 << 40) if args.path == "ll" else "0"
-    if args.path == "two_shot":
-        os.environ["GDRAA_RB_MAX_BYTES"] = "0"
     out = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
 
@@ -84,8 +81,6 @@ def main():
         w0 = torch.randn(n, device=dev, generator=torch.Generator(device=dev).manual_seed(7))
         if args.path == "ll" and gdraa.gdraa_small_step_bytes(world, code) < nbytes:
             break                                          # the shard no longer fits a slot
-        if args.path == "rb" and gdraa.gdraa_rb_message_bytes(world) < nbytes:
-            break                                          # above the receive-buffer limit
         w = w0.clone()
         v = torch.zeros(n, device=dev)
         gdraa.gdraa_register(w)
