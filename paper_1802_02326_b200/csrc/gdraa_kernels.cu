@@ -901,7 +901,9 @@ struct TmaCfg {
     static constexpr bool UPD = MODE != kMean;
     static constexpr int PER_EL = WORLD * SG + (UPD ? 8 : 0);      // smem bytes / element
     static constexpr int BUDGET = STAGE_KB * 1024;
-    static constexpr int CH = BUDGET / PER_EL >= 2048 ? 2048 : (BUDGET / PER_EL >= 1024 ? 1024 : 512);
+    // 4096-element chunks only for stage budgets above the library's 40 KB (tune sweeps)
+    static constexpr int CH = (STAGE_KB > 40 && BUDGET / PER_EL >= 4096) ? 4096
+                              : (BUDGET / PER_EL >= 2048 ? 2048 : (BUDGET / PER_EL >= 1024 ? 1024 : 512));
     static constexpr int STAGES = ST_;
     static constexpr int CW = CW_;                                 // consumer warps
     static constexpr int THREADS = 32 * (CW + 1);
@@ -913,10 +915,10 @@ struct TmaCfg {
 // mean and the mixed-precision model copy -- so that every destination gets one 16-byte
 // store per thread and step, else 4).
 template <typename TG, int WORLD, int MODE, int CW_ = 16, int ST_ = 4, int TAILDIV_ = 4,
-          int TDEPTH_ = ST_, int ROT_ = 0, int VE_ = 0>
-__global__ void __launch_bounds__(TmaCfg<TG, WORLD, MODE, CW_, ST_, TAILDIV_, TDEPTH_, ROT_>::THREADS, 1)
+          int TDEPTH_ = ST_, int ROT_ = 0, int VE_ = 0, int SKB_ = 40>
+__global__ void __launch_bounds__(TmaCfg<TG, WORLD, MODE, CW_, ST_, TAILDIV_, TDEPTH_, ROT_, SKB_>::THREADS, 1)
 gdraa_tma_kernel(const __grid_constant__ KParams p) {
-    using C = TmaCfg<TG, WORLD, MODE, CW_, ST_, TAILDIV_, TDEPTH_, ROT_>;
+    using C = TmaCfg<TG, WORLD, MODE, CW_, ST_, TAILDIV_, TDEPTH_, ROT_, SKB_>;
     using EL = Elem<TG>;
     using Raw = typename EL::Raw;
     constexpr bool kUpdate = C::UPD;

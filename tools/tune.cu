@@ -213,10 +213,10 @@ void lsu(int cap = 0) {
 }
 
 template <typename TG, int WORLD, int MODE, int CW, int ST, int TD = 4, int TDEP = ST, int ROT = 0,
-          int VE = 0>
+          int VE = 0, int SKB = 40>
 void tma(int cap = 0) {
-    using C = TmaCfg<TG, WORLD, MODE, CW, ST, TD, TDEP, ROT>;
-    auto fn = gdraa_tma_kernel<TG, WORLD, MODE, CW, ST, TD, TDEP, ROT, VE>;
+    using C = TmaCfg<TG, WORLD, MODE, CW, ST, TD, TDEP, ROT, SKB>;
+    auto fn = gdraa_tma_kernel<TG, WORLD, MODE, CW, ST, TD, TDEP, ROT, VE, SKB>;
     CK(cudaFuncSetAttribute(reinterpret_cast<const void *>(fn),
                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     int per = 0;
@@ -227,8 +227,8 @@ void tma(int cap = 0) {
                                      (uint64_t)sm_count() * per);
     if (cap > 0) gx = std::min<uint64_t>(gx, cap);
     char shape[64];
-    std::snprintf(shape, sizeof shape, "CW%d_ST%d_CH%d_TD%d_TDEP%d_ROT%d_VE%d_per%d", CW, ST,
-                  C::CH, TD, C::TDEPTH, ROT, VE, per);
+    std::snprintf(shape, sizeof shape, "CW%d_ST%d_CH%d_TD%d_TDEP%d_ROT%d_VE%d_SKB%d_per%d", CW,
+                  ST, C::CH, TD, C::TDEPTH, ROT, VE, SKB, per);
     run<TG, WORLD, MODE>(fn, C::THREADS, C::SMEM, (int)std::max<uint64_t>(gx, 1), "tma", shape);
 }
 
@@ -275,6 +275,15 @@ void sweep() {
                 tma<TG, WORLD, MODE, 16, 4, 4, 4, 0, 4>();
                 tma<TG, WORLD, MODE, 16, 4, 4, 4, 0, 8>();
             }
+    } else if (WHAT == "stage") {
+        // chunk size (stage bytes) x ring depth, twice interleaved; the library: 40 KB x 4
+        for (int rep = 0; rep < 2; ++rep) {
+            tma<TG, WORLD, MODE, 16, 4, 4, 4, 0, 0, 40>();
+            tma<TG, WORLD, MODE, 16, 5, 4, 5, 0, 0, 40>();
+            tma<TG, WORLD, MODE, 16, 3, 4, 3, 0, 0, 64>();
+            tma<TG, WORLD, MODE, 16, 2, 4, 2, 0, 0, 100>();
+            tma<TG, WORLD, MODE, 16, 6, 4, 6, 0, 0, 28>();
+        }
     } else if (WHAT == "mc") {
         // the library's TMA shape: unicast, multicast all-gather, multicast barriers, both;
         // twice, interleaved
@@ -378,7 +387,7 @@ static void setup_multicast() {
 
 int main(int argc, char **argv) {
     if (argc < 5) {
-        std::fprintf(stderr, "usage: tune <world> <L> <f32|bf16> <sgd|mp|mean> [iters] [lib|lsu|tma|tail|ctas|solo|mc|ve]\n");
+        std::fprintf(stderr, "usage: tune <world> <L> <f32|bf16> <sgd|mp|mean> [iters] [lib|lsu|tma|tail|ctas|solo|mc|ve|stage]\n");
         return 1;
     }
     W = std::atoi(argv[1]);
