@@ -30,13 +30,15 @@ struct alignas(128) Pad {
     uint64_t ll_calls;             // calls served by the small-message (LL) path
     uint64_t mc_calls;             // calls that used the multicast barrier (tools/tune.cu A/B)
     uint64_t _p3[10];
-    // Distributed exit (kFlagDistExit, experimental): every CTA of sender p adds the
+#ifdef GDRAA_EXPERIMENTAL
+    // Distributed exit (kFlagDistExit, tools/tune.cu only): every CTA of sender p adds the
     // elements it finished (pulled, folded, pushed) to recv_done[p] of every peer after its
     // fence; the owner's last CTA waits until recv_done[p] reaches recv_expect[p] + len_p.
     uint64_t recv_done[kMaxWorld];     // written by peers (remote atomics)
     uint64_t _p4[16 - kMaxWorld];
     uint64_t recv_expect[kMaxWorld];   // written by the owner's last CTA
     uint64_t _p5[16 - kMaxWorld];
+#endif
 };
 static_assert(sizeof(Pad) % 128 == 0, "pad layout");
 
