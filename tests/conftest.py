@@ -26,3 +26,20 @@ def golden():
     import json
     with open(os.path.join(ROOT, "tests", "golden", "spec_examples.json")) as f:
         return json.load(f)
+
+
+def mp_world():
+    """World size of the multi-process tests: one rank per visible GPU (at most 8), or two
+    ranks sharing the only GPU -- separate processes and CUDA contexts, time-sliced by
+    the GPU -- so that a one-GPU box still runs the cross-process path (job server, CUDA
+    IPC mappings, cross-process flag barriers), if not NVLink."""
+    import torch
+    return max(2, min(torch.cuda.device_count(), 8))
+
+
+def rank_device(rank):
+    """Select and return the device of `rank` in a multi-process test (rank mod GPUs)."""
+    import torch
+    d = rank % torch.cuda.device_count()
+    torch.cuda.set_device(d)
+    return f"cuda:{d}"

@@ -1,6 +1,11 @@
 """Multi-process parity over NVLink: one process per GPU, job server control plane,
 CUDA-IPC peer mappings, the fused kernel pulling/pushing peer memory.  Runs with
-world = number of visible GPUs (2 or 4 under `gpurun --gpus N`); skipped on 1 GPU."""
+world = number of visible GPUs (2 or 4 under `gpurun --gpus N`) over NVLink; on a one-GPU
+box (the driver's round-end configuration) with world 2, both ranks on the one GPU as
+separate processes and CUDA contexts, time-sliced (tests.conftest.mp_world): no NVLink,
+but every other part of the multi-process path -- job server, IPC mappings of
+caching-allocator blocks, cross-process release/acquire flags, bulk copies from
+IPC-mapped addresses, IterDone/IterStart -- runs as it does across GPUs."""
 import json
 import os
 
@@ -9,11 +14,10 @@ import pytest
 import torch
 import torch.multiprocessing as mp
 
-from tests.conftest import has_cuda
+from tests.conftest import has_cuda, mp_world
 
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu,
-              pytest.mark.skipif(not has_cuda() or torch.cuda.device_count() < 2,
-                                 reason="needs >= 2 GPUs")]
+              pytest.mark.skipif(not has_cuda(), reason="needs a GPU")]
 
 
 def _worker(rank, world, sock, L_list, out_dir):
@@ -25,8 +29,8 @@ def _worker(rank, world, sock, L_list, out_dir):
     from tests._parity import compare
     from tests.test_gpu_parity import from_dev, make_grads, to_dev
 
-    torch.cuda.set_device(rank)
-    dev = f"cuda:{rank}"
+    from tests.conftest import rank_device
+    dev = rank_device(rank)
     os.environ["GDRAA_JOBSERVER"] = sock
     gdraa.gdraa_init(world, rank)
     report = {"rank": rank, "cases": 0}
@@ -116,7 +120,7 @@ def _worker(rank, world, sock, L_list, out_dir):
 
 def test_multiprocess_parity(tmp_path):
     from paper_1802_02326_b200 import jobserver
-    world = min(torch.cuda.device_count(), 8)
+    world = mp_world()
     sock = str(tmp_path / "js.sock")
     js = jobserver.start(world, sock)
     L_list = [1, 1000, 70_001, 1 << 20]
@@ -147,8 +151,8 @@ def _gated_worker(rank, world, sock, out_dir):
     from tests._parity import compare
     from tests.test_gpu_parity import from_dev, make_grads, to_dev
 
-    torch.cuda.set_device(rank)
-    dev = f"cuda:{rank}"
+    from tests.conftest import rank_device
+    dev = rank_device(rank)
     os.environ["GDRAA_JOBSERVER"] = sock
     gdraa.gdraa_init(world, rank)
     calls = 0
@@ -177,7 +181,7 @@ def _gated_worker(rank, world, sock, out_dir):
 
 def test_multiprocess_gated(tmp_path):
     from paper_1802_02326_b200 import jobserver
-    world = min(torch.cuda.device_count(), 8)
+    world = mp_world()
     sock = str(tmp_path / "js.sock")
     js = jobserver.start(world, sock, gated=True)
     try:
@@ -205,8 +209,8 @@ def _bucket_worker(rank, world, sock, out_dir):
     from tests._parity import compare
     from tests.test_gpu_parity import from_dev, make_grads, to_dev
 
-    torch.cuda.set_device(rank)
-    dev = f"cuda:{rank}"
+    from tests.conftest import rank_device
+    dev = rank_device(rank)
     os.environ["GDRAA_JOBSERVER"] = sock
     gdraa.gdraa_init(world, rank)
     L = 1_048_576
@@ -248,7 +252,7 @@ def _bucket_worker(rank, world, sock, out_dir):
 
 def test_multiprocess_bucketed_ranges(tmp_path):
     from paper_1802_02326_b200 import jobserver
-    world = min(torch.cuda.device_count(), 8)
+    world = mp_world()
     sock = str(tmp_path / "js.sock")
     js = jobserver.start(world, sock)
     try:
@@ -268,8 +272,8 @@ def _ls_worker(rank, world, sock, out_dir):
     from synth.least_squares import Problem
     from tests.test_gpu_training import serial_trajectory
 
-    torch.cuda.set_device(rank)
-    dev = f"cuda:{rank}"
+    from tests.conftest import rank_device
+    dev = rank_device(rank)
     os.environ["GDRAA_JOBSERVER"] = sock
     gdraa.gdraa_init(world, rank)
     P = Problem(seed=5)
@@ -296,7 +300,7 @@ def _ls_worker(rank, world, sock, out_dir):
 
 def test_multiprocess_least_squares_ssgd(tmp_path):
     from paper_1802_02326_b200 import jobserver
-    world = min(torch.cuda.device_count(), 8)
+    world = mp_world()
     sock = str(tmp_path / "js.sock")
     js = jobserver.start(world, sock)
     try:
@@ -354,8 +358,8 @@ def _full_worker(rank, world, sock, out_dir):
     from tests._parity import compare
     from tests.test_gpu_parity import from_dev, to_dev
 
-    torch.cuda.set_device(rank)
-    dev = f"cuda:{rank}"
+    from tests.conftest import rank_device
+    dev = rank_device(rank)
     os.environ["GDRAA_JOBSERVER"] = sock
     gdraa.gdraa_init(world, rank)
     lr, mom, wd = synth.PAPER_LR, synth.PAPER_MOM, 0.001
@@ -419,7 +423,7 @@ def test_multiprocess_full_size_sampled(tmp_path):
     steps, bit-exact on windows at every shard boundary, the ragged end, the all-ranks
     -0.0 segment (AMB-3) and random places."""
     from paper_1802_02326_b200 import jobserver
-    world = min(torch.cuda.device_count(), 8)
+    world = mp_world()
     sock = str(tmp_path / "js.sock")
     js = jobserver.start(world, sock)
     try:

@@ -1,4 +1,5 @@
-"""Failure handling over real processes (>= 2 GPUs): a peer that never arrives makes the
+"""Failure handling over real processes (one per GPU; on a one-GPU box both ranks share
+it, time-sliced -- tests.conftest.mp_world): a peer that never arrives makes the
 kernel give up after GDRAA_TIMEOUT_MS and every later call report GDRAA_ETIMEOUT naming
 the missing rank ("peer-timeout ... names the missing ranks"); a peer process that
 dies is seen by the job server (socket EOF), whose abort flag -- mapped into the
@@ -14,8 +15,7 @@ import torch.multiprocessing as mp
 from tests.conftest import has_cuda
 
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu,
-              pytest.mark.skipif(not has_cuda() or torch.cuda.device_count() < 2,
-                                 reason="needs >= 2 GPUs")]
+              pytest.mark.skipif(not has_cuda(), reason="needs a GPU")]
 
 
 def _setup(rank, world, sock, timeout_ms, n):
@@ -23,10 +23,10 @@ def _setup(rank, world, sock, timeout_ms, n):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     os.environ["GDRAA_JOBSERVER"] = sock
     os.environ["GDRAA_TIMEOUT_MS"] = str(timeout_ms)
-    torch.cuda.set_device(rank)
+    from tests.conftest import rank_device
+    dev = rank_device(rank)
     from paper_1802_02326_b200 import gdraa
     gdraa.gdraa_init(world, rank)
-    dev = f"cuda:{rank}"
     w = torch.zeros(n, device=dev)
     g = torch.ones(n, device=dev)
     v = torch.zeros(n, device=dev)
@@ -113,7 +113,8 @@ def _mismatch_worker(rank, world, sock, out):
     os.environ["GDRAA_JOBSERVER"] = sock
     # rank 1 would serve small steps with the two-shot kernel, rank 0 with the LL kernel
     os.environ["GDRAA_LL_SGD_MAX_BYTES"] = "0" if rank == 1 else str(1 << 20)
-    torch.cuda.set_device(rank)
+    from tests.conftest import rank_device
+    rank_device(rank)
     from paper_1802_02326_b200 import gdraa
     res = {"rank": rank}
     try:
