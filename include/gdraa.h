@@ -181,6 +181,42 @@ int gdraa_sgd_step_mp_range(float *w_master, void *w_model, const void *g, float
                             gdraa_stream_t s);
 
 /*
+ * Bucket sets (SURVEY §8(f) NEXT-3 "keeping two syncs per bucket-set"; P:189 the
+ * synchronizations come "as late as the DL needs"; Alg. 1 line 153 = the 1st
+ * synchronization, line 166 = the 2nd).  The calls of one iteration's buckets each need
+ * their own 2nd synchronization -- bucket k may be reduced only once every rank's
+ * backward has produced it -- but the 1st (every peer's broadcast into our buffers has
+ * landed, every peer has finished reading our g) is needed only before the next forward
+ * pass reads w and the next backward overwrites g.  Between gdraa_bucket_set_begin and
+ * gdraa_bucket_set_end every collective call (whole-buffer or _range, any mode) runs its
+ * 2nd synchronization and its data movement as usual but defers its 1st; _end performs
+ * one 1st synchronization for all of them.  A set of K two-shot calls thus counts K + 1
+ * device barriers in sync_waits instead of 2K (small-message calls, which carry both
+ * synchronisations with their data, are unchanged).
+ *
+ * gdraa_bucket_set_begin -- open a set (local, host only; enqueues nothing).
+ * Errors: ESTATE (not initialised, or a set is already open).
+ *
+ * gdraa_bucket_set_end -- close the set (collective: every rank closes it after the same
+ * calls).  Enqueues on s, ordered after every call of the set (the cross-stream rule
+ * above), one small kernel: a system-scope fence of the set's pushes, one exit flag to
+ * each peer, a wait for each peer's.  Nothing is enqueued at world 1.  Work after it on
+ * s sees every result of the set on every rank.
+ * Errors: ESTATE (no set open), ETIMEOUT (sticky), ECUDA.
+ *
+ * Inside a set:
+ *  - The results of a call (w / buf / w_model over its range; v and w_master on the
+ *    owner shard) are complete on every rank only after gdraa_bucket_set_end; do not
+ *    read them, or pass them to another call, before that.
+ *  - The calls of one set must write disjoint element ranges of every destination
+ *    buffer (EINVAL otherwise: an overlapping range would read data still in flight).
+ *  - g must not be overwritten before gdraa_bucket_set_end has completed (peers may
+ *    still be reading it).
+ */
+int gdraa_bucket_set_begin(void);
+int gdraa_bucket_set_end(gdraa_stream_t s);
+
+/*
  * gdraa_poly_lr -- the paper's "poly" learning-rate policy with "gamma is 1" read as
  * the power: lr0 * (1 - iter/max_iter)^power, in double, rounded
  * once to float; 0 for iter >= max_iter; -1 if max_iter == 0.  Pure host function.
@@ -229,7 +265,9 @@ size_t gdraa_small_step_bytes(int world, int dtype, int mixed);
 
 typedef struct {
     uint64_t calls;            /* collective calls completed on the device (device counter) */
-    uint64_t sync_waits;       /* device barrier completions: 2 per call when world >= 2     */
+    uint64_t sync_waits;       /* device barrier completions: 2 per call when world >= 2
+                                  (1 per call inside a bucket set, + 1 per
+                                  gdraa_bucket_set_end)                                      */
     uint64_t rs_bytes_in;      /* algorithmic reduce bytes pulled from peers (Eq. 2)         */
     uint64_t rs_bytes_out;     /* algorithmic reduce bytes peers pulled from us (Eq. 1)      */
     uint64_t ag_bytes_out;     /* algorithmic broadcast bytes pushed to peers                */
@@ -308,6 +346,14 @@ int gdraa_vr_sgd_step_mp_range(int world, float *const *w_master, void *const *w
                                const void *const *g, float *const *v, size_t n, int dtype,
                                size_t first, size_t count, float lr, float mom, float wd,
                                gdraa_stream_t s);
+
+/*
+ * Bucket sets over virtual ranks (the semantics of gdraa_bucket_set_begin / _end for the
+ * gdraa_vr_* calls of this `world` on the current device; one open set per world).
+ * Errors: EINVAL (world), ESTATE (set already open / not open), ECUDA, ETIMEOUT.
+ */
+int gdraa_vr_bucket_set_begin(int world);
+int gdraa_vr_bucket_set_end(int world, gdraa_stream_t s);
 
 #ifdef __cplusplus
 }

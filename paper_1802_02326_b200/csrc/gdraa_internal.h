@@ -104,6 +104,10 @@ constexpr uint32_t kFlagCtaFence = 1u;
 // directly how many elements it finished (measured slower: DESIGN.md §11).
 constexpr uint32_t kFlagMcPeersOnly = 2u;
 constexpr uint32_t kFlagDistExit = 4u;
+// kFlagDeferExit: the call is inside a bucket set (gdraa_bucket_set_begin/_end): the
+// two-shot kernels skip the exit fence and the exit flag exchange (they still run the
+// entry barrier); launch_gdraa_exit performs the set's single 1st synchronization.
+constexpr uint32_t kFlagDeferExit = 8u;
 uint32_t env_kernel_flags();
 constexpr int kModes = 3;
 
@@ -111,6 +115,10 @@ constexpr int kModes = 3;
 // cooperative: use cudaLaunchCooperativeKernel (required when vr_rows > 1).
 cudaError_t launch_gdraa(const KParams &p, int dtype, int mode, int vr_rows,
                          bool cooperative, cudaStream_t s, int *grid_x_out);
+
+// The deferred exit barrier of a bucket set: fence + exit-flag exchange at the epoch of
+// the last call, one 32-thread CTA per (virtual) rank (vr_rows = gridDim.y).
+cudaError_t launch_gdraa_exit(const KParams &p, int vr_rows, bool cooperative, cudaStream_t s);
 
 // Max co-resident CTAs of the kernel for (dtype, mode, world) on this device.
 int max_ctas(int dtype, int mode, int world);

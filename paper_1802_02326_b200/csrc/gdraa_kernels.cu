@@ -463,12 +463,15 @@ gdraa_kernel(const __grid_constant__ KParams p) {
     // Our pushes must be performed system-wide before the peers hear of them.  Either
     // every thread fences its own stores, or (kFlagCtaFence) the CTA synchronises and
     // one thread fences for all of them (release cumulativity over bar.sync).
-    // N = 1: the kernel boundary orders our stores.
+    // N = 1: the kernel boundary orders our stores.  A call inside a bucket set
+    // (kFlagDeferExit) leaves both the fence and the flag exchange to the set's
+    // gdraa_exit_kernel.
+    const bool defer = (p.flags & kFlagDeferExit) != 0;
     const bool cta_fence = (p.flags & kFlagCtaFence) != 0;
-    if (WORLD > 1 && !cta_fence) fence_acq_rel_sys();
+    if (WORLD > 1 && !cta_fence && !defer) fence_acq_rel_sys();
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (WORLD > 1 && cta_fence) fence_acq_rel_sys();
+        if (WORLD > 1 && cta_fence && !defer) fence_acq_rel_sys();
         const unsigned prev = atomicAdd(&mine->arrive, 1u);
         s_last = (prev == gridDim.x - 1);
         if (s_last) __threadfence();
@@ -476,7 +479,7 @@ gdraa_kernel(const __grid_constant__ KParams p) {
     __syncthreads();
     if (!s_last) return;
     if (threadIdx.x == 0) GDRAA_STAMP(3);
-    if (WORLD > 1) {
+    if (WORLD > 1 && !defer) {
         if (threadIdx.x < WORLD && threadIdx.x != rank)
             st_release_sys(&p.pad[vr][threadIdx.x]->exit[rank], epoch);
         if (threadIdx.x < WORLD && threadIdx.x != rank) {
@@ -493,7 +496,7 @@ gdraa_kernel(const __grid_constant__ KParams p) {
         mine->arrive = 0;
         mine->next = 0;
         mine->calls += 1;
-        if (WORLD > 1) mine->sync_waits += 2;
+        if (WORLD > 1) mine->sync_waits += defer ? 1 : 2;
         mine->epoch = epoch;
         if (p.done[vr] != nullptr) *p.done[vr] = epoch;   // job-server "IterDone" flag
     }
@@ -1195,11 +1198,12 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
 #else
     constexpr bool dist = false;
 #endif
+    const bool defer = (p.flags & kFlagDeferExit) != 0 && !dist && !mcb;   // bucket set
     const bool cta_fence = (p.flags & kFlagCtaFence) != 0 || dist;
-    if (WORLD > 1 && !cta_fence) fence_acq_rel_sys();
+    if (WORLD > 1 && !cta_fence && !defer) fence_acq_rel_sys();
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (WORLD > 1 && cta_fence) fence_acq_rel_sys();
+        if (WORLD > 1 && cta_fence && !defer) fence_acq_rel_sys();
 #ifdef GDRAA_EXPERIMENTAL
         if (dist) {
             if (blockIdx.x == gridDim.x - 1) my_elems += len - lenv;   // the ragged tail
@@ -1246,7 +1250,7 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
         if (s_abort) return;
     } else
 #endif
-    if (WORLD > 1) {
+    if (WORLD > 1 && !defer) {
         if (threadIdx.x < WORLD && threadIdx.x != rank)
             st_release_sys(&p.pad[vr][threadIdx.x]->exit[rank], epoch);
         if (threadIdx.x < WORLD && threadIdx.x != rank) {
@@ -1263,11 +1267,43 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
         mine->arrive = 0;
         mine->next = 0;
         mine->calls += 1;
-        if (WORLD > 1) mine->sync_waits += 2;
+        if (WORLD > 1) mine->sync_waits += defer ? 1 : 2;
         if (mcb) mine->mc_calls += 1;
         mine->epoch = epoch;
         if (p.done[vr] != nullptr) *p.done[vr] = epoch;
     }
+}
+
+// ---------------------------------------------------------------------------------
+// The deferred 1st synchronization of a bucket set (gdraa_bucket_set_end; SURVEY §8(f)
+// NEXT-3, "as late as the DL needs").  The set's two-shot calls ran their entry
+// barrier and data movement but neither fenced nor exchanged exit flags; this grid,
+// stream-ordered after all of them, performs both once: every pushing thread of those
+// kernels has finished (kernel boundary), a system-scope fence makes their stores
+// performed, and each rank tells every peer and waits for every peer with the epoch of
+// the set's last call (exit flags are monotone, so the skipped epochs need no flag of
+// their own).  One CTA of 32 threads per (virtual) rank; the epoch is not advanced.
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(32) gdraa_exit_kernel(const __grid_constant__ KParams p) {
+    const int vr = blockIdx.y;
+    const int rank = p.rank0 + vr;
+    Pad *mine = p.pad[vr][rank];
+    __shared__ int s_abort;
+    if (threadIdx.x == 0) s_abort = 0;
+    const uint64_t epoch = *reinterpret_cast<volatile uint64_t *>(&mine->epoch);
+    __syncthreads();
+    const int q = threadIdx.x;
+    if (q < p.world && q != rank) {
+        fence_acq_rel_sys();
+        st_release_sys(&p.pad[vr][q]->exit[rank], epoch);
+        if (!wait_geq(&mine->exit[q], epoch, p.timeout_ns, p.abort)) {
+            report_timeout(p.err, 2, q, vr);
+            s_abort = 1;
+        }
+    }
+    __syncthreads();
+    if (s_abort) return;
+    if (threadIdx.x == 0) mine->sync_waits += 1;
 }
 
 using KernelFnLL = void (*)(KParams);
@@ -1436,6 +1472,17 @@ Launch pick(int dtype, int mode, int world) {
 }
 
 }  // namespace
+
+cudaError_t launch_gdraa_exit(const KParams &p, int vr_rows, bool cooperative, cudaStream_t s) {
+    dim3 grid(1, vr_rows), block(32);
+    if (cooperative) {
+        void *args[] = {const_cast<KParams *>(&p)};
+        return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(gdraa_exit_kernel),
+                                           grid, block, args, 0, s);
+    }
+    gdraa_exit_kernel<<<grid, block, 0, s>>>(p);
+    return cudaGetLastError();
+}
 
 int max_ctas(int dtype, int mode, int world) {
     Launch l = pick(dtype, mode, world);

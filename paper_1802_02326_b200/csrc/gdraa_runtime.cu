@@ -137,6 +137,31 @@ struct StreamOrder {
     bool have = false;
 };
 
+// A bucket set (gdraa_bucket_set_begin / _end): the calls inside it skip their exit
+// barrier, so their results are complete only at _end; they must therefore write disjoint
+// destination ranges.  spans = the [lo, hi) byte ranges written so far in the open set.
+struct BucketSet {
+    bool open = false;
+    std::vector<std::pair<uintptr_t, uintptr_t>> spans;
+};
+
+int set_check(const BucketSet &b, const void *dst, size_t bytes) {
+    if (!b.open) return GDRAA_OK;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(dst), hi = lo + bytes;
+    for (const auto &sp : b.spans)
+        if (lo < sp.second && sp.first < hi)
+            return fail(GDRAA_EINVAL, "bucket set: destination range %p + %zu bytes overlaps "
+                        "a range written earlier in the set (results are complete only at "
+                        "gdraa_bucket_set_end)", dst, bytes);
+    return GDRAA_OK;
+}
+
+void set_note(BucketSet &b, const void *dst, size_t bytes) {
+    if (!b.open) return;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(dst);
+    b.spans.emplace_back(lo, lo + bytes);
+}
+
 struct State {
     bool inited = false;
     int world = 0, rank = 0, device = 0;
@@ -161,6 +186,7 @@ struct State {
     uint64_t issued = 0;
     // Cross-stream ordering (see StreamOrder): every call shares this rank's pad and LL slots.
     StreamOrder order;
+    BucketSet set;                      // open bucket set (deferred exit barriers)
     bool fatal = false;
     int fatal_code = 0;
     std::string fatal_msg;
@@ -350,7 +376,7 @@ void fill_common(KParams &p, uint64_t n) {
     }
     p.ll_pairs = g.ll_pairs;
     p.ll_sleep_ns = static_cast<uint32_t>(env_u64("GDRAA_LL_SLEEP_NS", 256));
-    p.flags = env_kernel_flags();
+    p.flags = env_kernel_flags() | (g.set.open ? kFlagDeferExit : 0u);
     p.err = g.err_d;
     // IterDone: the last CTA's store into the host-mapped page costs nothing measurable
     // (profiles/r69_alpha.json: two-shot sgd sweep with and without it within 0.2 us)
@@ -412,6 +438,7 @@ struct VrDevice {
     uint64_t ll_pairs[kMaxWorld + 1] = {};
     ErrBlock *err_h = nullptr, *err_d = nullptr;
     StreamOrder order;                  // virtual-rank calls share these pads too
+    BucketSet set[kMaxWorld + 1];       // open bucket set per world (gdraa_vr_bucket_set_*)
 };
 
 }  // namespace
@@ -550,8 +577,15 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
     p.err = d->err_d;
     p.ll_pairs = d->ll[world] != nullptr ? d->ll_pairs[world] : 0;
     p.ll_sleep_ns = static_cast<uint32_t>(env_u64("GDRAA_LL_SLEEP_NS", 256));
-    p.flags = env_kernel_flags();
+    BucketSet &set = d->set[world];
+    p.flags = env_kernel_flags() | (set.open ? kFlagDeferExit : 0u);
     const size_t es = dtype == GDRAA_F32 ? 4 : 2;
+    const size_t ed = mode == kSgd ? 4 : (mode == kSgdMp ? 2 : es);
+    for (int q = 0; q < world; ++q) {
+        rc = set_check(set, dst[q], n * ed);
+        if (rc) return rc;
+    }
+    for (int q = 0; q < world; ++q) set_note(set, dst[q], n * ed);
     rc = order_after_previous(d->order, s);
     if (rc) return rc;
     if (mode == kMean && world > 1 && n * es <= 8 * p.ll_pairs) {   // latency path
@@ -838,6 +872,8 @@ static int mean_common(void *buf, size_t first, size_t count, gdraa_stream_t s) 
     rc = wait_go();
     if (rc) return rc;
     const size_t es = elem_size(r->dtype);
+    rc = set_check(g.set, offset_ptr(r->local, first, es), count * es);
+    if (rc) return rc;
     KParams p;
     fill_common(p, count);
     for (int q = 0; q < g.world; ++q) {
@@ -857,6 +893,7 @@ static int mean_common(void *buf, size_t first, size_t count, gdraa_stream_t s) 
         if (rc) return rc;
     }
     account(count, r->dtype, 0);
+    set_note(g.set, offset_ptr(r->local, first, es), count * es);
     return note_launch(g.order, cs);
 }
 
@@ -897,6 +934,8 @@ static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, 
     rc = wait_go();
     if (rc) return rc;
     const size_t eg = elem_size(rg->dtype), ew = elem_size(rw->dtype);
+    rc = set_check(g.set, offset_ptr(rw->local, first, ew), count * ew);
+    if (rc) return rc;
     KParams p;
     fill_common(p, count);
     p.lr = lr;
@@ -922,6 +961,7 @@ static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, 
         if (rc) return rc;
     }
     account(count, rg->dtype, mode == kSgd ? 4 : 2);
+    set_note(g.set, offset_ptr(rw->local, first, ew), count * ew);
     return note_launch(g.order, cs);
 }
 
@@ -950,6 +990,35 @@ int gdraa_sgd_step_mp_range(float *w_master, void *w_model, const void *gr, floa
                             gdraa_stream_t s) {
     if (count == SIZE_MAX) return fail(GDRAA_EINVAL, "count out of range");
     return sgd_common(kSgdMp, w_master, w_model, gr, v, first, count, lr, mom, wd, s);
+}
+
+int gdraa_bucket_set_begin(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.inited) return fail(GDRAA_ESTATE, "gdraa_init has not been called");
+    if (g.set.open) return fail(GDRAA_ESTATE, "a bucket set is already open");
+    g.set.open = true;
+    g.set.spans.clear();
+    return GDRAA_OK;
+}
+
+int gdraa_bucket_set_end(gdraa_stream_t s) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.inited) return fail(GDRAA_ESTATE, "gdraa_init has not been called");
+    if (!g.set.open) return fail(GDRAA_ESTATE, "no bucket set is open");
+    g.set.open = false;
+    g.set.spans.clear();
+    int rc = check_sticky();
+    if (rc) return rc;
+    if (g.world == 1) return GDRAA_OK;     // no barrier to defer
+    KParams p;
+    fill_common(p, 1);
+    const cudaStream_t cs = reinterpret_cast<cudaStream_t>(s);
+    rc = order_after_previous(g.order, cs);
+    if (rc) return rc;
+    cudaError_t e = launch_gdraa_exit(p, 1, false, cs);
+    if (e != cudaSuccess) return fail(GDRAA_ECUDA, "exit kernel launch: %s", cudaGetErrorString(e));
+    g.host.launches += 1;
+    return note_launch(g.order, cs);
 }
 
 float gdraa_poly_lr(float lr0, uint64_t iter, uint64_t max_iter, float power) {
@@ -1081,6 +1150,44 @@ int gdraa_vr_sgd_step_mp_range(int world, float *const *w_master, void *const *w
     std::lock_guard<std::mutex> lk(g_mu);
     VrArgs a{world, g_, w_model, v, w_master, n, dtype, lr, mom, wd, kSgdMp};
     return vr_range(a, first, count, reinterpret_cast<cudaStream_t>(s));
+}
+
+int gdraa_vr_bucket_set_begin(int world) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (world < 1 || world > kMaxWorld) return fail(GDRAA_EINVAL, "world %d out of [1,%d]", world, kMaxWorld);
+    VrDevice *d = nullptr;
+    int rc = vr_prepare(world, &d);
+    if (rc) return rc;
+    if (d->set[world].open) return fail(GDRAA_ESTATE, "a bucket set is already open (world %d)", world);
+    d->set[world].open = true;
+    d->set[world].spans.clear();
+    return GDRAA_OK;
+}
+
+int gdraa_vr_bucket_set_end(int world, gdraa_stream_t s) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (world < 1 || world > kMaxWorld) return fail(GDRAA_EINVAL, "world %d out of [1,%d]", world, kMaxWorld);
+    VrDevice *d = nullptr;
+    int rc = vr_prepare(world, &d);
+    if (rc) return rc;
+    if (!d->set[world].open) return fail(GDRAA_ESTATE, "no bucket set is open (world %d)", world);
+    d->set[world].open = false;
+    d->set[world].spans.clear();
+    if (world == 1) return GDRAA_OK;
+    KParams p;
+    std::memset(&p, 0, sizeof p);
+    p.world = world;
+    p.rank0 = 0;
+    p.timeout_ns = env_u64("GDRAA_TIMEOUT_MS", 30000) * 1000000ull;
+    for (int r = 0; r < world; ++r)
+        for (int q = 0; q < world; ++q) p.pad[r][q] = d->pads[world] + q;
+    p.err = d->err_d;
+    const cudaStream_t cs = reinterpret_cast<cudaStream_t>(s);
+    rc = order_after_previous(d->order, cs);
+    if (rc) return rc;
+    cudaError_t e = launch_gdraa_exit(p, world, true, cs);
+    if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr exit kernel launch: %s", cudaGetErrorString(e));
+    return note_launch(d->order, cs);
 }
 
 }  // extern "C"

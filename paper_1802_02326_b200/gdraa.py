@@ -29,7 +29,8 @@ EXPORTED = ["gdraa_sgd_step_ex", "gdraa_sgd_step_mp", "gdraa_poly_lr",
             "gdraa_shard", "gdraa_get_stats", "gdraa_finalize", "gdraa_last_error",
             "gdraa_version", "gdraa_vr_allreduce_mean", "gdraa_vr_sgd_step",
             "gdraa_vr_allreduce_mean_range", "gdraa_vr_sgd_step_range",
-            "gdraa_vr_sgd_step_mp_range"]
+            "gdraa_vr_sgd_step_mp_range", "gdraa_bucket_set_begin", "gdraa_bucket_set_end",
+            "gdraa_vr_bucket_set_begin", "gdraa_vr_bucket_set_end"]
 
 
 class GdraaError(RuntimeError):
@@ -85,6 +86,10 @@ _sig = {
     "gdraa_vr_sgd_step_mp_range": ([_i, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                                     ctypes.POINTER(_vp), ctypes.POINTER(_vp), _sz, _i, _sz, _sz,
                                     _f, _f, _f, _vp], _i),
+    "gdraa_bucket_set_begin": ([], _i),
+    "gdraa_bucket_set_end": ([_vp], _i),
+    "gdraa_vr_bucket_set_begin": ([_i], _i),
+    "gdraa_vr_bucket_set_end": ([_i, _vp], _i),
 }
 for _name, (_args, _res) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -196,6 +201,14 @@ def gdraa_sgd_step_mp_range(w_master, w_model, g, v, first: int, count: int, lr:
            "gdraa_sgd_step_mp_range")
 
 
+def gdraa_bucket_set_begin():
+    _check(_lib.gdraa_bucket_set_begin(), "gdraa_bucket_set_begin")
+
+
+def gdraa_bucket_set_end(stream=None):
+    _check(_lib.gdraa_bucket_set_end(_stream(stream)), "gdraa_bucket_set_end")
+
+
 def gdraa_small_message_bytes(world: int) -> int:
     return int(_lib.gdraa_small_message_bytes(world))
 
@@ -292,3 +305,11 @@ def gdraa_vr_sgd_step_mp_range(w_master, w_model, g, v, first: int, count: int, 
                                            _ptr_array(g), _ptr_array(v), n, dtype_code(g[0]),
                                            first, count, lr, mom, wd, _stream(stream)),
            "gdraa_vr_sgd_step_mp_range")
+
+
+def gdraa_vr_bucket_set_begin(world: int):
+    _check(_lib.gdraa_vr_bucket_set_begin(world), "gdraa_vr_bucket_set_begin")
+
+
+def gdraa_vr_bucket_set_end(world: int, stream=None):
+    _check(_lib.gdraa_vr_bucket_set_end(world, _stream(stream)), "gdraa_vr_bucket_set_end")

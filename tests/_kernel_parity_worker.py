@@ -51,6 +51,18 @@ def main():
                     compare(from_dev(wm_d[r])[off:off + ln], w_exp[off:off + ln], "f32",
                             what="mp master")
                     compare(from_dev(bufs[r]), mean_exp, dt, what="mean")
+                # the same step as two buckets inside a bucket set (deferred exit barrier)
+                w_d = [to_dev(w0) for _ in range(N)]
+                v_d = [to_dev(v0) for _ in range(N)]
+                half = L // 2 // 8 * 8
+                gdraa.gdraa_vr_bucket_set_begin(N)
+                for first, cnt in ((half, L - half), (0, half)):
+                    if cnt:
+                        gdraa.gdraa_vr_sgd_step_range(w_d, g_d, v_d, first, cnt, 0.1, 0.9, 0.001)
+                gdraa.gdraa_vr_bucket_set_end(N)
+                torch.cuda.synchronize()
+                for r in range(N):
+                    compare(from_dev(w_d[r]), w_exp, "f32", what=f"set w N={N} {dt} L={L} r{r}")
                 count += 1
     print(f"OK {os.environ.get('GDRAA_KERNEL')} {count} cases")
 

@@ -80,11 +80,22 @@ def test_shard_rejects(args):
 
 def test_calls_before_init_fail_cleanly():
     for fn, args in [(gdraa.gdraa_register, (1 << 20, 10, 0)), (gdraa.gdraa_get_stats, ()),
-                     (gdraa.gdraa_finalize, ()), (gdraa.gdraa_deregister, (1 << 20,))]:
+                     (gdraa.gdraa_finalize, ()), (gdraa.gdraa_deregister, (1 << 20,)),
+                     (gdraa.gdraa_bucket_set_begin, ()), (gdraa.gdraa_bucket_set_end, (0,))]:
         with pytest.raises(gdraa.GdraaError) as e:
             fn(*args)
         assert e.value.name == "GDRAA_ESTATE", fn
     assert "gdraa_init" in gdraa.gdraa_last_error()
+
+
+@pytest.mark.parametrize("world", [0, 9, -1])
+def test_vr_bucket_set_rejects_world(world):
+    """World is checked before any device work (no GPU needed)."""
+    for fn, args in [(gdraa.gdraa_vr_bucket_set_begin, (world,)),
+                     (gdraa.gdraa_vr_bucket_set_end, (world, 0))]:
+        with pytest.raises(gdraa.GdraaError) as e:
+            fn(*args)
+        assert e.value.name == "GDRAA_EINVAL", fn
 
 
 def test_failed_init_leaves_clean_state():

@@ -543,6 +543,89 @@ def test_vr_bucketed_ranges(N, dt):
         compare(from_dev(bufs[r]), m_exp, dt, what=f"bucketed mean N={N} r{r}")
 
 
+@pytest.mark.parametrize("N", [2, 3, 4, 8])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_vr_bucket_set(N, dt):
+    """NEXT-3 "two syncs per bucket-set": the same out-of-order buckets inside one bucket
+    set -- every two-shot call skips its exit barrier, gdraa_vr_bucket_set_end runs one
+    for all of them -- give the whole-buffer oracle step, for sgd, the mixed-precision
+    step and the mean (three destination buffers in the same set, LL and two-shot calls
+    mixed), and a second set right after the first sees the first set's results."""
+    bf16 = dt == "bf16"
+    L = 5_000_017
+    buckets = _buckets(L)
+    gs = make_grads("like", 900 + N, N, L, bf16)
+    w0, v0 = synth.w_like(900 + N, L), synth.w_like(950 + N, L)
+    wd, lr, mom = 0.001, synth.PAPER_LR, synth.PAPER_MOM
+    w1, v1 = oracle.sgd_step_wd(gs, w0, v0, lr, mom, wd)
+    w2, v2 = oracle.sgd_step_wd(gs, w1, v1, lr, mom, wd)
+    wm_exp, vm_exp, m_exp = oracle.sgd_step_wd(gs, w0, v0, lr, mom, wd, model_dtype=oracle.BF16)
+    mean_exp = oracle.allreduce_mean(gs)
+    g_d = [to_dev(g, bf16) for g in gs]
+    w_d = [to_dev(w0) for _ in range(N)]
+    v_d = [to_dev(v0) for _ in range(N)]
+    wm_d = [to_dev(w0) for _ in range(N)]
+    vm_d = [to_dev(v0) for _ in range(N)]
+    model_d = [torch.zeros(L, dtype=torch.bfloat16, device=DEV) for _ in range(N)]
+    bufs = [to_dev(g, bf16) for g in gs]
+    for it in range(2):                  # two iterations = two sets, chained through w, v
+        gdraa.gdraa_vr_bucket_set_begin(N)
+        for first, count in buckets:
+            gdraa.gdraa_vr_sgd_step_range(w_d, g_d, v_d, first, count, lr, mom, wd)
+            if it == 0:
+                gdraa.gdraa_vr_sgd_step_mp_range(wm_d, model_d, g_d, vm_d, first, count, lr,
+                                                 mom, wd)
+                gdraa.gdraa_vr_allreduce_mean_range(bufs, first, count)
+        gdraa.gdraa_vr_bucket_set_end(N)
+        if it == 0:
+            torch.cuda.synchronize()
+            for r in range(N):
+                compare(from_dev(w_d[r]), w1, "f32", what=f"set w it0 N={N} r{r}")
+                compare(from_dev(model_d[r]), m_exp, "bf16", what=f"set mp model N={N} r{r}")
+                compare(from_dev(bufs[r]), mean_exp, dt, what=f"set mean N={N} r{r}")
+    torch.cuda.synchronize()
+    for r in range(N):
+        compare(from_dev(w_d[r]), w2, "f32", what=f"set w it1 N={N} r{r}")
+        vh, wmh, vmh, vmask = from_dev(v_d[r]), from_dev(wm_d[r]), from_dev(vm_d[r]), np.zeros(L, bool)
+        for first, count in buckets:
+            off, ln = gdraa.gdraa_shard(N, r, count)
+            vmask[first + off:first + off + ln] = True
+        compare(vh[vmask], v2[vmask], "f32", what=f"set v N={N} r{r}")
+        compare(wmh[vmask], wm_exp[vmask], "f32", what=f"set mp master N={N} r{r}")
+        compare(vmh[vmask], vm_exp[vmask], "f32", what=f"set mp v N={N} r{r}")
+
+
+def test_vr_bucket_set_rules():
+    """Set state errors and the disjoint-destination rule inside a set."""
+    N, L = 2, 1 << 16
+    w = [torch.zeros(L, device=DEV) for _ in range(N)]
+    g = [torch.ones(L, device=DEV) for _ in range(N)]
+    v = [torch.zeros(L, device=DEV) for _ in range(N)]
+    with pytest.raises(gdraa.GdraaError) as e:
+        gdraa.gdraa_vr_bucket_set_end(N)
+    assert e.value.name == "GDRAA_ESTATE"
+    for bad in (0, 9):
+        with pytest.raises(gdraa.GdraaError) as e:
+            gdraa.gdraa_vr_bucket_set_begin(bad)
+        assert e.value.name == "GDRAA_EINVAL"
+    gdraa.gdraa_vr_bucket_set_begin(N)
+    with pytest.raises(gdraa.GdraaError) as e:
+        gdraa.gdraa_vr_bucket_set_begin(N)
+    assert e.value.name == "GDRAA_ESTATE"
+    gdraa.gdraa_vr_sgd_step_range(w, g, v, 0, 1024, 0.5, 0.0)
+    with pytest.raises(gdraa.GdraaError) as e:       # overlaps [0, 1024) of the same w
+        gdraa.gdraa_vr_sgd_step_range(w, g, v, 1016, 64, 0.5, 0.0)
+    assert e.value.name == "GDRAA_EINVAL" and "overlaps" in str(e.value)
+    gdraa.gdraa_vr_sgd_step_range(w, g, v, 1024, L - 1024, 0.5, 0.0)   # disjoint: fine
+    gdraa.gdraa_vr_bucket_set_end(N)
+    torch.cuda.synchronize()
+    for r in range(N):                    # w = 0 - 0.5 * mean(1) everywhere, once
+        assert torch.equal(w[r], torch.full((L,), -0.5, device=DEV))
+    gdraa.gdraa_vr_sgd_step_range(w, g, v, 0, 1024, 0.5, 0.0)          # outside a set
+    torch.cuda.synchronize()
+    assert torch.equal(w[0][:1024], torch.full((1024,), -1.0, device=DEV))
+
+
 def test_vr_range_rejects_bad_ranges():
     N, L = 2, 1000
     w = [torch.zeros(L, device=DEV) for _ in range(N)]

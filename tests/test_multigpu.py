@@ -245,6 +245,49 @@ def _bucket_worker(rank, world, sock, out_dir):
         compare(from_dev(buf), oracle.allreduce_mean(gs), dt, what=f"bucketed mean {dt}")
         for t in (w, g, buf):
             gdraa.gdraa_deregister(t)
+    # a bucket set (NEXT-3, "two syncs per bucket-set"): the two-shot buckets skip their
+    # exit barrier, gdraa_bucket_set_end runs one for the set; two chained iterations
+    L2 = 6_048_576
+    set_buckets = [(3_000_000, 3_000_000), (6_000_000, 48_576), (0, 3_000_000)]
+    for dt in ("f32", "bf16"):
+        bf16 = dt == "bf16"
+        es = 2 if bf16 else 4
+        gs = make_grads("like", 63, world, L2, bf16)
+        w0, v0 = synth.w_like(63, L2), synth.w_like(64, L2)
+        w1, v1 = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, 0.001)
+        w2, v2 = oracle.sgd_step_wd(gs, w1, v1, 0.1, 0.9, 0.001)
+        g = to_dev(gs[rank], bf16, dev)
+        w, v = to_dev(w0, dev=dev), to_dev(v0, dev=dev)
+        gdraa.gdraa_register(w)
+        gdraa.gdraa_register(g)
+        lim = gdraa.gdraa_small_step_bytes(world, gdraa.GDRAA_BF16 if bf16 else gdraa.GDRAA_F32)
+        two_shot = sum(c * es > lim for _, c in set_buckets)
+        assert 0 < two_shot < len(set_buckets)
+        st0 = gdraa.gdraa_get_stats()
+        for it in range(2):
+            gdraa.gdraa_bucket_set_begin()
+            for first, count in set_buckets:
+                done = torch.cuda.Event()
+                done.record(torch.cuda.current_stream())
+                side.wait_event(done)
+                gdraa.gdraa_sgd_step_range(w, g, v, first, count, 0.1, 0.9, 0.001, stream=side)
+            gdraa.gdraa_bucket_set_end(stream=side)
+            torch.cuda.current_stream().wait_stream(side)
+            if it == 0:
+                torch.cuda.synchronize()
+                compare(from_dev(w), w1, "f32", what=f"set w it0 {dt} r{rank}")
+        torch.cuda.synchronize()
+        compare(from_dev(w), w2, "f32", what=f"set w it1 {dt} r{rank}")
+        vh = from_dev(v)
+        for first, count in set_buckets:
+            off, ln = gdraa.gdraa_shard(world, rank, count)
+            a, b = first + off, first + off + ln
+            compare(vh[a:b], v2[a:b], "f32", what=f"set v {dt} r{rank}")
+        st1 = gdraa.gdraa_get_stats()
+        # per set: one entry barrier per two-shot bucket + the set's single exit barrier
+        assert st1["sync_waits"] - st0["sync_waits"] == 2 * (two_shot + 1), (st0, st1)
+        for t in (w, g):
+            gdraa.gdraa_deregister(t)
     gdraa.gdraa_finalize()
     with open(os.path.join(out_dir, f"bucket{rank}.ok"), "w") as f:
         f.write("ok")

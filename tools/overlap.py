@@ -28,6 +28,9 @@ def main():
     ap.add_argument("--buckets", type=int, default=8)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--gemm", type=int, default=0, help="GEMM size (0: calibrate)")
+    ap.add_argument("--set", action="store_true",
+                    help="issue the buckets of one iteration as a bucket set "
+                         "(gdraa_bucket_set_begin/_end: one deferred exit barrier per set)")
     args = ap.parse_args()
     out = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
@@ -106,16 +109,24 @@ def main():
     evs = [torch.cuda.Event() for _ in range(K)]
 
     def overlap():
+        if args.set:
+            gdraa.gdraa_bucket_set_begin()
         for k, (first, count) in enumerate(buckets):
             torch.mm(A, A, out=C)               # "produces" bucket k
             evs[k].record(main_s)
             side.wait_event(evs[k])
             gdraa.gdraa_sgd_step_range(w, g, v, first, count, lr, mom, 0.0, stream=side)
+        if args.set:
+            gdraa.gdraa_bucket_set_end(stream=side)
         main_s.wait_stream(side)
 
     def comm_buckets():
+        if args.set:
+            gdraa.gdraa_bucket_set_begin()
         for first, count in buckets:
             gdraa.gdraa_sgd_step_range(w, g, v, first, count, lr, mom, 0.0)
+        if args.set:
+            gdraa.gdraa_bucket_set_end()
 
     t_bwd = timed(bwd, args.iters)
     t_comm_b = timed(comm_buckets, args.iters)
@@ -125,7 +136,7 @@ def main():
         hidden = (t_serial - t_overlap) / min(t_bwd, t_comm)
         line = {"n_gpus": world, "L": L, "buckets": K, "gemm_n": n,
                 "max_ctas": os.environ.get("GDRAA_MAX_CTAS", "all"),
-                "kernel": os.environ.get("GDRAA_KERNEL", "lsu"),
+                "kernel": os.environ.get("GDRAA_KERNEL", "default"), "bucket_set": args.set,
                 "bwd_us": t_bwd * 1e3, "comm_us": t_comm * 1e3,
                 "comm_bucketed_us": t_comm_b * 1e3, "serial_us": t_serial * 1e3,
                 "overlap_us": t_overlap * 1e3, "speedup": t_serial / t_overlap,
