@@ -212,6 +212,8 @@ int gdraa_sgd_step_mp_range(float *w_master, void *w_model, const void *g, float
  *    buffer (EINVAL otherwise: an overlapping range would read data still in flight).
  *  - g must not be overwritten before gdraa_bucket_set_end has completed (peers may
  *    still be reading it).
+ *  - gdraa_finalize with a set still open runs the set's exit barrier first (so that
+ *    the peers' gdraa_bucket_set_end completes), then leaves as usual.
  */
 int gdraa_bucket_set_begin(void);
 int gdraa_bucket_set_end(gdraa_stream_t s);

@@ -585,25 +585,26 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
         rc = set_check(set, dst[q], n * ed);
         if (rc) return rc;
     }
-    for (int q = 0; q < world; ++q) set_note(set, dst[q], n * ed);
     rc = order_after_previous(d->order, s);
     if (rc) return rc;
+    cudaError_t e;
+    const char *what;
     if (mode == kMean && world > 1 && n * es <= 8 * p.ll_pairs) {   // latency path
-        cudaError_t e = launch_gdraa_ll(p, dtype, world, true, s);
-        if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr LL launch: %s", cudaGetErrorString(e));
-        return note_launch(d->order, s);
+        e = launch_gdraa_ll(p, dtype, world, true, s);
+        what = "vr LL launch";
+    } else if (upd && world > 1 && n * es <= ll_sgd_limit_bytes(world) &&
+               ll_sgd_fits(p.blk, dtype, mode, p.ll_pairs)) {   // small-message SGD step
+        e = launch_gdraa_ll_sgd(p, dtype, mode, world, true, s);
+        what = "vr LL SGD launch";
+    } else {
+        int gx = 0;
+        e = use_tma_kernel(dtype, mode, world)
+                ? launch_gdraa_tma(p, dtype, mode, world, true, s, &gx)
+                : launch_gdraa(p, dtype, mode, world, true, s, &gx);
+        what = "vr kernel launch";
     }
-    if (upd && world > 1 && n * es <= ll_sgd_limit_bytes(world) &&
-        ll_sgd_fits(p.blk, dtype, mode, p.ll_pairs)) {   // small-message SGD step
-        cudaError_t e = launch_gdraa_ll_sgd(p, dtype, mode, world, true, s);
-        if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr LL SGD launch: %s", cudaGetErrorString(e));
-        return note_launch(d->order, s);
-    }
-    int gx = 0;
-    cudaError_t e = use_tma_kernel(dtype, mode, world)
-                        ? launch_gdraa_tma(p, dtype, mode, world, true, s, &gx)
-                                     : launch_gdraa(p, dtype, mode, world, true, s, &gx);
-    if (e != cudaSuccess) return fail(GDRAA_ECUDA, "vr kernel launch: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess) return fail(GDRAA_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    for (int q = 0; q < world; ++q) set_note(set, dst[q], n * ed);
     return note_launch(d->order, s);
 }
 
@@ -1048,6 +1049,16 @@ int gdraa_finalize(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g.inited) return fail(GDRAA_ESTATE, "gdraa_init has not been called");
     int rc = GDRAA_OK;
+    if (g.set.open && g.world > 1 && !g.fatal) {
+        // a bucket set left open: run its deferred exit barrier so that the peers'
+        // gdraa_bucket_set_end (which waits for ours) completes
+        KParams p;
+        fill_common(p, 1);
+        if (cudaDeviceSynchronize() != cudaSuccess ||
+            launch_gdraa_exit(p, 1, false, nullptr) != cudaSuccess)
+            rc = fail(GDRAA_ECUDA, "exit kernel launch at finalize");
+    }
+    g.set.open = false;
     cudaError_t se = cudaDeviceSynchronize();
     {
         int st = check_sticky();

@@ -306,6 +306,53 @@ def test_multiprocess_bucketed_ranges(tmp_path):
     assert all((tmp_path / f"bucket{r}.ok").exists() for r in range(world))
 
 
+def _open_set_worker(rank, world, sock, out_dir):
+    """Rank 0 closes its bucket set; every other rank calls gdraa_finalize with the set
+    still open, which must run the deferred exit barrier so that rank 0's completes."""
+    import sys
+    import time
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_1802_02326_b200 import gdraa
+    from tests.conftest import rank_device
+
+    dev = rank_device(rank)
+    os.environ["GDRAA_JOBSERVER"] = sock
+    os.environ["GDRAA_TIMEOUT_MS"] = "20000"
+    gdraa.gdraa_init(world, rank)
+    L = 4_000_000                                      # two-shot at every world size
+    w = torch.zeros(L, device=dev)
+    g = torch.ones(L, device=dev)
+    v = torch.zeros(L, device=dev)
+    gdraa.gdraa_register(w)
+    gdraa.gdraa_register(g)
+    gdraa.gdraa_bucket_set_begin()
+    gdraa.gdraa_sgd_step_range(w, g, v, 0, L, 0.5, 0.0)
+    t0 = time.time()
+    if rank == 0:
+        gdraa.gdraa_bucket_set_end()
+        torch.cuda.synchronize()
+        assert bool((w == -0.5).all())
+    gdraa.gdraa_finalize()
+    with open(os.path.join(out_dir, f"open{rank}.json"), "w") as f:
+        json.dump({"s": time.time() - t0}, f)
+
+
+def test_finalize_closes_an_open_bucket_set(tmp_path):
+    from paper_1802_02326_b200 import jobserver
+    world = mp_world()
+    sock = str(tmp_path / "js.sock")
+    js = jobserver.start(world, sock)
+    try:
+        mp.start_processes(_open_set_worker, args=(world, sock, str(tmp_path)), nprocs=world,
+                           join=True, start_method="spawn")
+    finally:
+        out, _ = js.communicate(timeout=120)
+    line = json.loads(out.strip().splitlines()[-1])["jobserver"]
+    assert line["ok"], line
+    for r in range(world):
+        assert json.load(open(tmp_path / f"open{r}.json"))["s"] < 15
+
+
 def _ls_worker(rank, world, sock, out_dir):
     """NEXT-4 over real processes: each rank computes its own b-sample least-squares
     gradient and steps through gdraa_sgd_step; rank 0 checks the serial trajectory."""
