@@ -439,7 +439,7 @@ def _window_grads(seed, world, a, L, bf16):
     return out
 
 
-def _full_worker(rank, world, sock, out_dir):
+def _full_worker(rank, world, sock, out_dir, configs=None):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import oracle
@@ -454,7 +454,7 @@ def _full_worker(rank, world, sock, out_dir):
     gdraa.gdraa_init(world, rank)
     lr, mom, wd = synth.PAPER_LR, synth.PAPER_MOM, 0.001
     checked = 0
-    for name, dt, mp_ in FULL:
+    for name, dt, mp_ in (configs or FULL):
         L = synth.L_R50 if name == "r50" else synth.L_R101
         bf16 = dt == "bf16"
         assert L * (2 if bf16 else 4) > gdraa.gdraa_small_step_bytes(world)   # two-shot
@@ -521,6 +521,27 @@ def test_multiprocess_full_size_sampled(tmp_path):
                            join=True, start_method="spawn")
     finally:
         js.communicate(timeout=120)
+    for r in range(world):
+        assert json.load(open(tmp_path / f"full{r}.json"))["checked"] > 0
+
+
+def test_multiprocess_config4_world8(tmp_path):
+    """Config 4 as BASELINE.json states it -- ResNet-50 bf16 gradients, fp32 accumulation
+    and master weights, 8 ranks -- at full size through the multi-process path (+ the
+    NEXT-1 bf16 model-copy form), two chained steps, sampled windows bit-exact against the
+    oracle.  Eight processes on whatever GPUs the box has (time-sliced when fewer than 8)."""
+    from paper_1802_02326_b200 import jobserver
+    world = 8
+    sock = str(tmp_path / "js.sock")
+    js = jobserver.start(world, sock)
+    cfg = [("r50", "bf16", False), ("r50", "bf16", True)]
+    try:
+        mp.start_processes(_full_worker, args=(world, sock, str(tmp_path), cfg), nprocs=world,
+                           join=True, start_method="spawn")
+    finally:
+        out, _ = js.communicate(timeout=300)
+    line = json.loads(out.strip().splitlines()[-1])["jobserver"]
+    assert line["ok"] and line["ranks_joined"] == 8 and line["data_bytes"] == 0, line
     for r in range(world):
         assert json.load(open(tmp_path / f"full{r}.json"))["checked"] > 0
 
