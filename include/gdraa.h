@@ -219,6 +219,33 @@ int gdraa_bucket_set_begin(void);
 int gdraa_bucket_set_end(gdraa_stream_t s);
 
 /*
+ * gdraa_bucket_set_begin_streamed -- open a STREAMED bucket set: the same semantics as
+ * gdraa_bucket_set_begin (results complete at gdraa_bucket_set_end, disjoint destination
+ * ranges), served by ONE persistent kernel instead of one kernel per call.  The set's
+ * first call launches that kernel, with `ctas` CTAs per rank, on a stream of the
+ * library's own (ordered after the previous collective); each call then only describes
+ * its bucket with three stream memory operations (cuStreamWriteValue64) on the caller's
+ * stream, which take effect when that stream reaches the call -- i.e. when the bucket's
+ * gradient is final -- and the kernel reduces, updates and broadcasts each bucket as its
+ * description arrives, in call order, with one entry barrier per bucket and one exit
+ * barrier for the set.  No launch, grid drain or exit barrier per bucket.
+ *   ctas: >= 1, capped at the co-resident maximum.  The kernel holds these SMs until the
+ *         set ends, so they must leave enough SMs to the work that produces the buckets
+ *         (e.g. 32 of 148 beside a backward pass).
+ * Rules beyond gdraa_bucket_set_begin's:
+ *  - every call of the set uses the buffers, mode (mean / sgd / mp), gradient dtype and
+ *    lr / mom / wd of its first call (EINVAL otherwise); at most 511 calls per set;
+ *  - every call is served by the two-shot data path (the small-message kernels are not
+ *    used inside a streamed set); the results are the same bits;
+ *  - nothing may wait for the set's completion before gdraa_bucket_set_end has been
+ *    issued (the kernel is still waiting for buckets): no cudaDeviceSynchronize, no wait
+ *    on the set's streams; gdraa_get_stats returns ESTATE while such a set is open;
+ *  - not available in gated mode (ESTATE); world 1 behaves as gdraa_bucket_set_begin.
+ * Errors: ESTATE (not initialised, set already open, gated), EINVAL (ctas < 1), ECUDA.
+ */
+int gdraa_bucket_set_begin_streamed(int ctas);
+
+/*
  * gdraa_poly_lr -- the paper's "poly" learning-rate policy with "gamma is 1" read as
  * the power: lr0 * (1 - iter/max_iter)^power, in double, rounded
  * once to float; 0 for iter >= max_iter; -1 if max_iter == 0.  Pure host function.
@@ -356,6 +383,9 @@ int gdraa_vr_sgd_step_mp_range(int world, float *const *w_master, void *const *w
  */
 int gdraa_vr_bucket_set_begin(int world);
 int gdraa_vr_bucket_set_end(int world, gdraa_stream_t s);
+/* The streamed form for virtual ranks: one cooperative persistent launch of ctas x world
+ * CTAs serves the set's gdraa_vr_* calls (rules of gdraa_bucket_set_begin_streamed). */
+int gdraa_vr_bucket_set_begin_streamed(int world, int ctas);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,25 @@ struct ErrBlock {
     volatile int32_t vrank;                  // the (virtual) rank that timed out
 };
 
+// Streamed bucket sets (gdraa_bucket_set_begin_streamed): one persistent kernel serves
+// every bucket of the set.  The host describes bucket k with stream memory operations
+// on the caller's stream (so they take effect when the caller's stream reaches the call,
+// i.e. once the bucket's gradient is final): first[k], count[k], then ready[k] =
+// set_tag(gen, k); gdraa_bucket_set_end posts ready[K] = set_close(gen).  Tags carry the
+// set's generation, so values left from earlier sets are never mistaken for this one's.
+constexpr int kSetMax = 512;
+struct SetDesc {
+    uint64_t ready[kSetMax];
+    uint64_t first[kSetMax];
+    uint64_t count[kSetMax];
+};
+__host__ __device__ constexpr uint64_t set_tag(uint32_t gen, uint32_t k) {
+    return (static_cast<uint64_t>(gen) << 32) | (k + 1u);
+}
+__host__ __device__ constexpr uint64_t set_close(uint32_t gen) {
+    return (static_cast<uint64_t>(gen) << 32) | 0xFFFFFFFFu;
+}
+
 // Kernel parameters (passed by value).  Row vr describes virtual rank vr: one row in
 // multi-process mode (gridDim.y == 1, rank = rank0), `world` rows in the single-GPU
 // virtual-rank mode (gridDim.y == world, rank = blockIdx.y).
@@ -76,6 +95,11 @@ struct KParams {
     const volatile int32_t *abort;           // host-mapped job-server abort flag, or null:
                                              // spins give up early once a rank has died
     uint32_t flags;                          // kFlag* bits (launch-variant switches)
+    // streamed bucket set (gdraa_tma_set_kernel only): the bucket descriptors (shared by
+    // the virtual ranks of a vr launch), per-row chunk counters [kSetMax], the generation
+    const SetDesc *sdesc;
+    uint32_t *snext[kMaxWorld];
+    uint32_t sgen;
 #ifdef GDRAA_EXPERIMENTAL
     // Measured-and-rejected variants of the two-shot TMA kernel, compiled only into
     // tools/tune.cu for the A/B, never into the library.  NVLS multicast:
@@ -126,6 +150,11 @@ int max_ctas(int dtype, int mode, int world);
 // The TMA-staged variant of launch_gdraa (same semantics and results).
 cudaError_t launch_gdraa_tma(const KParams &p, int dtype, int mode, int vr_rows,
                              bool cooperative, cudaStream_t s, int *grid_x_out);
+// The persistent bucket-set kernel (world >= 2, any mode / dtype): p.dst / p.src / p.v /
+// p.wm are the BASE pointers of the buffers; buckets arrive through p.sdesc.  ctas: CTAs
+// per (virtual) rank (capped at the co-resident maximum).
+cudaError_t launch_gdraa_tma_set(const KParams &p, int dtype, int mode, int vr_rows,
+                                 bool cooperative, cudaStream_t s, int ctas);
 // Whether the runtime launches the TMA-staged kernel for this call (measured choice;
 // GDRAA_KERNEL=tma|lsu forces it).
 bool use_tma_kernel(int dtype, int mode, int world);

@@ -914,6 +914,143 @@ struct TmaCfg {
     static constexpr int SMEM = STAGES * STAGE_BYTES;
 };
 
+// a4 fold (+ a5 update) of one chunk that the TMA producer staged in shared memory, and
+// the a6 push; shared by gdraa_tma_kernel and gdraa_tma_set_kernel.  stage: the chunk's
+// stage (the N ranks' gradient blocks of CH elements, then w and v); g0c: index of the
+// chunk's first element relative to the base pointers p.dst[vr][*], vloc and wloc.
+template <typename C, typename TG, int WORLD, int MODE, int VE>
+__device__ __forceinline__ void tma_consume(const KParams &p, int vr, int rank,
+                                            const unsigned char *stage, uint64_t g0c,
+                                            uint32_t n_el, int ct, float *vloc, float *wloc,
+                                            float lr, float mom, float wd, void *mcd,
+                                            bool mc_self) {
+    using EL = Elem<TG>;
+    using Raw = typename EL::Raw;
+    constexpr bool kUpdate = C::UPD;
+    constexpr int H = VE / E;
+    using BfOut = typename std::conditional<H == 2, uint4, uint2>::type;   // VE bf16 values
+    auto src = [&](int q) { return reinterpret_cast<const TG *>(stage) + q * C::CH; };
+    const float *sw = reinterpret_cast<const float *>(stage + WORLD * C::SG * C::CH);
+    const float *sv = sw + C::CH;
+    for (uint32_t k = ct * VE; k < n_el; k += C::CW * 32 * VE) {
+        float m[H][E];
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            float x[WORLD][E];
+#pragma unroll
+            for (int q = 0; q < WORLD; ++q)
+                EL::widen(*reinterpret_cast<const Raw *>(src(q) + k + h * E), x[q]);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                float col[WORLD];
+#pragma unroll
+                for (int q = 0; q < WORLD; ++q) col[q] = x[q][e];
+                m[h][e] = average<WORLD>(col);
+            }
+        }
+        const uint64_t g0 = g0c + k;
+        if (kUpdate) {
+            float4 w[H];
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                w[h] = *reinterpret_cast<const float4 *>(sw + k + h * E);
+                float4 v = *reinterpret_cast<const float4 *>(sv + k + h * E);
+                sgd(m[h][0], lr, mom, wd, w[h].x, v.x);
+                sgd(m[h][1], lr, mom, wd, w[h].y, v.y);
+                sgd(m[h][2], lr, mom, wd, w[h].z, v.z);
+                sgd(m[h][3], lr, mom, wd, w[h].w, v.w);
+                st_vec(reinterpret_cast<uint4 *>(vloc + g0 + h * E), as_u4(v.x, v.y, v.z, v.w));
+            }
+            if (MODE == kSgd) {
+#pragma unroll
+                for (int h = 0; h < H; ++h) {
+                    const uint4 o = as_u4(w[h].x, w[h].y, w[h].z, w[h].w);
+                    const uint64_t gh = g0 + h * E;
+                    if (mcd != nullptr) {
+                        mc_st(reinterpret_cast<uint4 *>(static_cast<float *>(mcd) + gh), o);
+                        if (mc_self)
+                            st_vec(reinterpret_cast<uint4 *>(static_cast<float *>(p.dst[vr][rank]) + gh), o);
+                    } else {
+#pragma unroll
+                        for (int j = 1; j <= WORLD; ++j) {
+                            const int q = (rank + j) % WORLD;
+                            st_vec(reinterpret_cast<uint4 *>(static_cast<float *>(p.dst[vr][q]) + gh), o);
+                        }
+                    }
+                }
+            } else {   // kSgdMp: fp32 master shard stays local, bf16 copy to every rank
+                BfOut o;
+#pragma unroll
+                for (int h = 0; h < H; ++h) {
+                    st_vec(reinterpret_cast<uint4 *>(wloc + g0 + h * E),
+                           as_u4(w[h].x, w[h].y, w[h].z, w[h].w));
+                    const float wf[E] = {w[h].x, w[h].y, w[h].z, w[h].w};
+                    set_half(o, h, Elem<__nv_bfloat16>::narrow(wf));
+                }
+                if (mcd != nullptr) {
+                    mc_st_bf16(reinterpret_cast<BfOut *>(static_cast<__nv_bfloat16 *>(mcd) + g0), o);
+                    if (mc_self)
+                        st_vec(reinterpret_cast<BfOut *>(static_cast<__nv_bfloat16 *>(p.dst[vr][rank]) + g0), o);
+                } else {
+#pragma unroll
+                    for (int j = 1; j <= WORLD; ++j) {
+                        const int q = (rank + j) % WORLD;
+                        st_vec(reinterpret_cast<BfOut *>(static_cast<__nv_bfloat16 *>(p.dst[vr][q]) + g0), o);
+                    }
+                }
+            }
+        } else if constexpr (std::is_same<TG, float>::value) {
+            const Raw o = EL::narrow(m[0]);
+#pragma unroll
+            for (int j = 1; j <= WORLD; ++j) {
+                const int q = (rank + j) % WORLD;
+                st_vec(reinterpret_cast<Raw *>(static_cast<TG *>(p.dst[vr][q]) + g0), o);
+            }
+        } else {   // bf16 mean: VE elements -> one store per destination
+            BfOut o;
+#pragma unroll
+            for (int h = 0; h < H; ++h) set_half(o, h, EL::narrow(m[h]));
+#pragma unroll
+            for (int j = 1; j <= WORLD; ++j) {
+                const int q = (rank + j) % WORLD;
+                st_vec(reinterpret_cast<BfOut *>(static_cast<TG *>(p.dst[vr][q]) + g0), o);
+            }
+        }
+    }
+}
+
+// Scalar a3-a6 for elements e = lo, lo + stride, ... < hi (a shard's ragged tail of
+// len % 8 elements, which no 16-byte bulk copy covers), reading the ranks' gradients
+// directly; indices relative to the base pointers.
+template <typename TG, int WORLD, int MODE>
+__device__ __forceinline__ void tail_scalar(const KParams &p, int vr, int rank, uint64_t lo,
+                                            uint64_t hi, int stride, float *vloc, float *wloc,
+                                            float lr, float mom, float wd) {
+    using EL = Elem<TG>;
+    for (uint64_t e = lo; e < hi; e += stride) {
+        float col[WORLD];
+#pragma unroll
+        for (int q = 0; q < WORLD; ++q) col[q] = EL::load1(p.src[vr][q], e);
+        const float m = average<WORLD>(col);
+        if (MODE != kMean) {
+            float w = wloc[e], v = vloc[e];
+            sgd(m, lr, mom, wd, w, v);
+            vloc[e] = v;
+            if (MODE == kSgd) {
+                for (int j = 1; j <= WORLD; ++j)
+                    static_cast<float *>(p.dst[vr][(rank + j) % WORLD])[e] = w;
+            } else {
+                wloc[e] = w;
+                for (int j = 1; j <= WORLD; ++j)
+                    Elem<__nv_bfloat16>::store1(p.dst[vr][(rank + j) % WORLD], e, w);
+            }
+        } else {
+            for (int j = 1; j <= WORLD; ++j)
+                EL::store1(p.dst[vr][(rank + j) % WORLD], e, m);
+        }
+    }
+}
+
 // VE_: elements per consumer thread per step (0 = 8 when the broadcast is bf16 -- the bf16
 // mean and the mixed-precision model copy -- so that every destination gets one 16-byte
 // store per thread and step, else 4).
@@ -1073,120 +1210,15 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
             uint64_t e0;
             uint32_t n_el;
             chunk(c, e0, n_el);
-            for (uint32_t k = ct * VE; k < n_el; k += C::CW * 32 * VE) {
-                float m[H][E];
-#pragma unroll
-                for (int h = 0; h < H; ++h) {
-                    float x[WORLD][E];
-#pragma unroll
-                    for (int q = 0; q < WORLD; ++q)
-                        EL::widen(*reinterpret_cast<const Raw *>(stage_src(s, q) + k + h * E), x[q]);
-#pragma unroll
-                    for (int e = 0; e < E; ++e) {
-                        float col[WORLD];
-#pragma unroll
-                        for (int q = 0; q < WORLD; ++q) col[q] = x[q][e];
-                        m[h][e] = average<WORLD>(col);
-                    }
-                }
-                const uint64_t g0 = off + e0 + k;
-                if (kUpdate) {
-                    float4 w[H];
-#pragma unroll
-                    for (int h = 0; h < H; ++h) {
-                        w[h] = *reinterpret_cast<const float4 *>(stage_w(s) + k + h * E);
-                        float4 v = *reinterpret_cast<const float4 *>(stage_v(s) + k + h * E);
-                        sgd(m[h][0], lr, mom, wd, w[h].x, v.x);
-                        sgd(m[h][1], lr, mom, wd, w[h].y, v.y);
-                        sgd(m[h][2], lr, mom, wd, w[h].z, v.z);
-                        sgd(m[h][3], lr, mom, wd, w[h].w, v.w);
-                        st_vec(reinterpret_cast<uint4 *>(vloc + g0 + h * E), as_u4(v.x, v.y, v.z, v.w));
-                    }
-                    if (MODE == kSgd) {
-#pragma unroll
-                        for (int h = 0; h < H; ++h) {
-                            const uint4 o = as_u4(w[h].x, w[h].y, w[h].z, w[h].w);
-                            const uint64_t gh = g0 + h * E;
-                            if (mcd != nullptr) {
-                                mc_st(reinterpret_cast<uint4 *>(static_cast<float *>(mcd) + gh), o);
-                                if (mc_self)
-                                    st_vec(reinterpret_cast<uint4 *>(static_cast<float *>(p.dst[vr][rank]) + gh), o);
-                            } else {
-#pragma unroll
-                                for (int j = 1; j <= WORLD; ++j) {
-                                    const int q = (rank + j) % WORLD;
-                                    st_vec(reinterpret_cast<uint4 *>(static_cast<float *>(p.dst[vr][q]) + gh), o);
-                                }
-                            }
-                        }
-                    } else {   // kSgdMp: fp32 master shard stays local, bf16 copy to every rank
-                        BfOut o;
-#pragma unroll
-                        for (int h = 0; h < H; ++h) {
-                            st_vec(reinterpret_cast<uint4 *>(wloc + g0 + h * E),
-                                   as_u4(w[h].x, w[h].y, w[h].z, w[h].w));
-                            const float wf[E] = {w[h].x, w[h].y, w[h].z, w[h].w};
-                            set_half(o, h, Elem<__nv_bfloat16>::narrow(wf));
-                        }
-                        if (mcd != nullptr) {
-                            mc_st_bf16(reinterpret_cast<BfOut *>(static_cast<__nv_bfloat16 *>(mcd) + g0), o);
-                            if (mc_self)
-                                st_vec(reinterpret_cast<BfOut *>(static_cast<__nv_bfloat16 *>(p.dst[vr][rank]) + g0), o);
-                        } else {
-#pragma unroll
-                            for (int j = 1; j <= WORLD; ++j) {
-                                const int q = (rank + j) % WORLD;
-                                st_vec(reinterpret_cast<BfOut *>(static_cast<__nv_bfloat16 *>(p.dst[vr][q]) + g0), o);
-                            }
-                        }
-                    }
-                } else if constexpr (std::is_same<TG, float>::value) {
-                    const Raw o = EL::narrow(m[0]);
-#pragma unroll
-                    for (int j = 1; j <= WORLD; ++j) {
-                        const int q = (rank + j) % WORLD;
-                        st_vec(reinterpret_cast<Raw *>(static_cast<TG *>(p.dst[vr][q]) + g0), o);
-                    }
-                } else {   // bf16 mean: VE elements -> one store per destination
-                    BfOut o;
-#pragma unroll
-                    for (int h = 0; h < H; ++h) set_half(o, h, EL::narrow(m[h]));
-#pragma unroll
-                    for (int j = 1; j <= WORLD; ++j) {
-                        const int q = (rank + j) % WORLD;
-                        st_vec(reinterpret_cast<BfOut *>(static_cast<TG *>(p.dst[vr][q]) + g0), o);
-                    }
-                }
-            }
+            tma_consume<C, TG, WORLD, MODE, VE>(p, vr, rank, smem + s * C::STAGE_BYTES, off + e0,
+                                                n_el, ct, vloc, wloc, lr, mom, wd, mcd, mc_self);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
         }
         // ragged tail (len % 8 elements) by the last CTA's consumers, scalar
-        if (blockIdx.x == gridDim.x - 1) {
-            for (uint64_t t = lenv + ct; t < len; t += C::CW * 32) {
-                const uint64_t e = off + t;
-                float col[WORLD];
-#pragma unroll
-                for (int q = 0; q < WORLD; ++q) col[q] = EL::load1(p.src[vr][q], e);
-                const float m = average<WORLD>(col);
-                if (kUpdate) {
-                    float w = wloc[e], v = vloc[e];
-                    sgd(m, lr, mom, wd, w, v);
-                    vloc[e] = v;
-                    if (MODE == kSgd) {
-                        for (int j = 1; j <= WORLD; ++j)
-                            static_cast<float *>(p.dst[vr][(rank + j) % WORLD])[e] = w;
-                    } else {
-                        wloc[e] = w;
-                        for (int j = 1; j <= WORLD; ++j)
-                            Elem<__nv_bfloat16>::store1(p.dst[vr][(rank + j) % WORLD], e, w);
-                    }
-                } else {
-                    for (int j = 1; j <= WORLD; ++j)
-                        EL::store1(p.dst[vr][(rank + j) % WORLD], e, m);
-                }
-            }
-        }
+        if (blockIdx.x == gridDim.x - 1)
+            tail_scalar<TG, WORLD, MODE>(p, vr, rank, off + lenv + ct, off + len, C::CW * 32,
+                                         vloc, wloc, lr, mom, wd);
     }
 
     // a7: "1st synchronization" (as in gdraa_kernel)
@@ -1275,6 +1307,240 @@ gdraa_tma_kernel(const __grid_constant__ KParams p) {
 }
 
 // ---------------------------------------------------------------------------------
+// Streamed bucket set (gdraa_bucket_set_begin_streamed): ONE
+// persistent grid serves every bucket of an iteration, so a bucket costs neither a launch
+// nor a grid drain nor an exit barrier, and a CTA that runs out of work in bucket k moves
+// straight on to bucket k+1.  Per bucket k (descriptors written by stream memory
+// operations on the caller's stream when the bucket's gradient is final, see SetDesc):
+//   a2  the producer of every CTA waits for ready[k]; CTA 0 then stores epoch e_k into
+//       every peer's pad and every producer waits for every peer's e_k (the same flags as
+//       the per-call kernel, one epoch per bucket);
+//   a3-a6 chunks of the bucket's owner shard are claimed from next[k] and staged, folded,
+//       updated and pushed exactly as in gdraa_tma_kernel (tma_consume; the shard's
+//       ragged tail is one extra "chunk" done by scalar loads, tail_scalar);
+// and once the close marker arrives: a7 once for the whole set (per-CTA fence, the last
+// CTA exchanges exit flags at the last bucket's epoch).  Same arithmetic, same bits.
+// ---------------------------------------------------------------------------------
+template <typename TG, int WORLD, int MODE>
+__global__ void __launch_bounds__(TmaCfg<TG, WORLD, MODE>::THREADS, 1)
+gdraa_tma_set_kernel(const __grid_constant__ KParams p) {
+    using C = TmaCfg<TG, WORLD, MODE>;
+    constexpr bool kUpdate = C::UPD;
+    constexpr bool kBfOut = MODE == kSgdMp || (MODE == kMean && !std::is_same<TG, float>::value);
+    constexpr int VE = kBfOut ? 8 : 4;
+    constexpr uint32_t kDone = 0xFFFFFFFFu;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t full[C::STAGES], empty[C::STAGES];
+    __shared__ uint32_t s_bk[C::STAGES], s_chunk[C::STAGES];
+    __shared__ uint64_t s_first[C::STAGES], s_count[C::STAGES];
+    __shared__ int s_abort, s_last;
+    __shared__ uint32_t s_nb;
+
+    const int vr = blockIdx.y;
+    const int rank = p.rank0 + vr;
+    Pad *mine = p.pad[vr][rank];
+    const uint64_t epoch0 = *reinterpret_cast<volatile uint64_t *>(&mine->epoch);
+    if (threadIdx.x == 0) {
+        s_abort = 0;
+        s_nb = 0;
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    float *const vloc = p.v[vr];
+    float *const wloc = MODE == kSgdMp ? p.wm[vr] : static_cast<float *>(p.dst[vr][rank]);
+    constexpr uint64_t CHS = C::CH / C::TAILDIV;
+    // the owner shard of a bucket of `count` elements and its chunking (as gdraa_tma_kernel)
+    struct Geo {
+        uint64_t off, len, lenv, nbig, small0, nchunks;
+    };
+    auto geo = [&](uint64_t count) {
+        Geo g;
+        const uint64_t c = (count + WORLD - 1) / WORLD;
+        const uint64_t blk = (c + 63) / 64 * 64;
+        g.off = min(static_cast<uint64_t>(rank) * blk, count);
+        g.len = min(blk, count - g.off);
+        g.lenv = g.len & ~7ull;
+        const uint64_t tailv = 2ull * gridDim.x * CHS;
+        g.nbig = g.lenv > tailv ? (g.lenv - tailv) / C::CH : 0;
+        g.small0 = g.nbig * C::CH;
+        g.nchunks = g.nbig + (g.lenv - g.small0 + CHS - 1) / CHS;
+        return g;
+    };
+    auto chunk = [&](const Geo &g, uint32_t c, uint64_t &e0, uint32_t &n_el) {
+        if (c < g.nbig) {
+            e0 = static_cast<uint64_t>(c) * C::CH;
+            n_el = C::CH;
+        } else {
+            e0 = g.small0 + (c - g.nbig) * CHS;
+            n_el = static_cast<uint32_t>(g.lenv - e0 < CHS ? g.lenv - e0 : CHS);
+        }
+    };
+    auto stage_src = [&](int s, int q) {
+        return reinterpret_cast<TG *>(smem + s * C::STAGE_BYTES) + q * C::CH;
+    };
+    auto stage_w = [&](int s) {
+        return reinterpret_cast<float *>(smem + s * C::STAGE_BYTES + WORLD * C::SG * C::CH);
+    };
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0) {
+        if (lane == 0) {
+            // producer
+            const SetDesc *sd = p.sdesc;
+            uint32_t *next = p.snext[vr];
+            const uint64_t want_close = set_close(p.sgen);
+            uint32_t it = 0;
+            bool have_stage = false;
+            for (uint32_t b = 0; b < kSetMax; ++b) {
+                // bucket b described and its gradient final on this rank (or the set closed)
+                const uint64_t want = set_tag(p.sgen, b);
+                uint64_t r = ld_relaxed_sys(&sd->ready[b]);
+                if (r != want && r != want_close) {
+                    const uint64_t t0 = global_timer_ns();
+                    uint32_t polls = 0;
+                    while ((r = ld_relaxed_sys(&sd->ready[b])) != want && r != want_close) {
+                        if (global_timer_ns() - t0 > p.timeout_ns ||
+                            (p.abort != nullptr && (++polls & 4095u) == 0 && *p.abort != 0)) {
+                            report_timeout(p.err, 1, rank, vr);
+                            s_abort = 1;
+                            break;
+                        }
+                    }
+                    if (s_abort) break;
+                }
+                (void)ld_acquire_sys(&sd->ready[b]);
+                if (r == want_close) {
+                    s_nb = b;
+                    break;
+                }
+                const uint64_t first = *reinterpret_cast<const volatile uint64_t *>(&sd->first[b]);
+                const uint64_t count = *reinterpret_cast<const volatile uint64_t *>(&sd->count[b]);
+                // a2 for bucket b
+                const uint64_t e = epoch0 + 1 + b;
+                if (WORLD > 1) {
+                    if (blockIdx.x == 0)
+                        for (int q = 0; q < WORLD; ++q)
+                            if (q != rank) st_release_sys(&p.pad[vr][q]->entry[rank], e);
+                    for (int q = 0; q < WORLD && !s_abort; ++q)
+                        if (q != rank && !wait_geq(&mine->entry[q], e, p.timeout_ns, p.abort)) {
+                            report_timeout(p.err, 1, q, vr);
+                            s_abort = 1;
+                        }
+                    if (s_abort) break;
+                }
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                const Geo g = geo(count);
+                const uint32_t total = static_cast<uint32_t>(g.nchunks + (g.len > g.lenv ? 1 : 0));
+                for (;;) {
+                    const int s = it % C::STAGES;
+                    if (!have_stage) {
+                        if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+                        have_stage = true;
+                    }
+                    const uint32_t c = atomicAdd(&next[b], 1u);
+                    if (c >= total) break;               // bucket b done: keep the stage
+                    s_bk[s] = b;
+                    s_chunk[s] = c;
+                    s_first[s] = first;
+                    s_count[s] = count;
+                    if (c == g.nchunks) {
+                        mbar_arrive(&full[s]);            // ragged tail: no bulk copy
+                    } else {
+                        uint64_t e0;
+                        uint32_t n_el;
+                        chunk(g, c, e0, n_el);
+                        const uint64_t base = first + g.off + e0;
+                        mbar_arrive_tx(&full[s], n_el * C::PER_EL);
+#pragma unroll
+                        for (int q = 0; q < WORLD; ++q)
+                            bulk_g2s(stage_src(s, q), static_cast<const TG *>(p.src[vr][q]) + base,
+                                     n_el * C::SG, &full[s]);
+                        if (kUpdate) {
+                            bulk_g2s(stage_w(s), wloc + base, n_el * 4, &full[s]);
+                            bulk_g2s(stage_w(s) + C::CH, vloc + base, n_el * 4, &full[s]);
+                        }
+                    }
+                    ++it;
+                    have_stage = false;
+                }
+            }
+            // no more work: the consumers' stop sentinel
+            const int s = it % C::STAGES;
+            if (!have_stage && it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+            s_chunk[s] = kDone;
+            mbar_arrive(&full[s]);
+        }
+    } else {
+        const int ct = threadIdx.x - 32;
+        for (uint32_t it = 0;; ++it) {
+            const int s = it % C::STAGES;
+            mbar_wait(&full[s], (it / C::STAGES) & 1);
+            const uint32_t c = s_chunk[s];
+            if (c == kDone) break;
+            const uint64_t first = s_first[s];
+            const Geo g = geo(s_count[s]);
+            if (c == g.nchunks) {
+                if (ct < C::CW * 32)
+                    tail_scalar<TG, WORLD, MODE>(p, vr, rank, first + g.off + g.lenv + ct,
+                                                 first + g.off + g.len, C::CW * 32, vloc, wloc,
+                                                 p.lr, p.mom, p.wd);
+            } else {
+                uint64_t e0;
+                uint32_t n_el;
+                chunk(g, c, e0, n_el);
+                tma_consume<C, TG, WORLD, MODE, VE>(p, vr, rank, smem + s * C::STAGE_BYTES,
+                                                    first + g.off + e0, n_el, ct, vloc, wloc,
+                                                    p.lr, p.mom, p.wd, nullptr, false);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+    }
+
+    // a7 once for the set: our pushes performed, then the last CTA of this rank exchanges
+    // exit flags at the last bucket's epoch
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (WORLD > 1) fence_acq_rel_sys();
+        const unsigned prev = atomicAdd(&mine->arrive, 1u);
+        s_last = (prev == gridDim.x - 1);
+        if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (!s_last) return;
+    // every CTA's producer saw the same close index; take it from this one (or, after an
+    // abort, report nothing further: the error block already names the missing rank)
+    if (s_abort) return;
+    const uint32_t nb = s_nb;
+    const uint64_t e_last = epoch0 + nb;
+    if (WORLD > 1) {
+        if (threadIdx.x < WORLD && threadIdx.x != rank) {
+            st_release_sys(&p.pad[vr][threadIdx.x]->exit[rank], e_last);
+            if (!wait_geq(&mine->exit[threadIdx.x], e_last, p.timeout_ns, p.abort)) {
+                report_timeout(p.err, 2, threadIdx.x, vr);
+                s_abort = 1;
+            }
+        }
+        __syncthreads();
+        if (s_abort) return;
+    }
+    // reset the chunk counters this set used, for the next set
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) p.snext[vr][b] = 0;
+    if (threadIdx.x == 0) {
+        mine->arrive = 0;
+        mine->calls += nb;
+        if (WORLD > 1) mine->sync_waits += nb + 1;
+        mine->epoch = e_last;
+        if (p.done[vr] != nullptr) *p.done[vr] = e_last;
+    }
+}
+
+// ---------------------------------------------------------------------------------
 // The deferred 1st synchronization of a bucket set (gdraa_bucket_set_end; SURVEY §8(f)
 // NEXT-3, "as late as the DL needs").  The set's two-shot calls ran their entry
 // barrier and data movement but neither fenced nor exchanged exit flags; this grid,
@@ -1350,34 +1616,40 @@ struct TmaLaunch {
     int ch;
 };
 
-template <typename TG, int MODE, int WORLD>
+// SET: the persistent bucket-set kernel (world >= 2) instead of the per-call one
+template <typename TG, int MODE, int WORLD, bool SET>
 TmaLaunch pick_tma_w() {
     using C = TmaCfg<TG, WORLD, MODE>;
-    return {gdraa_tma_kernel<TG, WORLD, MODE>, C::THREADS, C::SMEM, C::CH};
-}
-
-template <typename TG, int MODE>
-TmaLaunch pick_tma_m(int world) {
-    switch (world) {
-        case 1: return pick_tma_w<TG, MODE, 1>();
-        case 2: return pick_tma_w<TG, MODE, 2>();
-        case 3: return pick_tma_w<TG, MODE, 3>();
-        case 4: return pick_tma_w<TG, MODE, 4>();
-        case 5: return pick_tma_w<TG, MODE, 5>();
-        case 6: return pick_tma_w<TG, MODE, 6>();
-        case 7: return pick_tma_w<TG, MODE, 7>();
-        case 8: return pick_tma_w<TG, MODE, 8>();
-        default: return {nullptr, 0, 0};
+    if constexpr (SET) {
+        if constexpr (WORLD < 2) return {nullptr, 0, 0, 0};
+        else return {gdraa_tma_set_kernel<TG, WORLD, MODE>, C::THREADS, C::SMEM, C::CH};
+    } else {
+        return {gdraa_tma_kernel<TG, WORLD, MODE>, C::THREADS, C::SMEM, C::CH};
     }
 }
 
-template <typename TG>
+template <typename TG, int MODE, bool SET>
+TmaLaunch pick_tma_m(int world) {
+    switch (world) {
+        case 1: return pick_tma_w<TG, MODE, 1, SET>();
+        case 2: return pick_tma_w<TG, MODE, 2, SET>();
+        case 3: return pick_tma_w<TG, MODE, 3, SET>();
+        case 4: return pick_tma_w<TG, MODE, 4, SET>();
+        case 5: return pick_tma_w<TG, MODE, 5, SET>();
+        case 6: return pick_tma_w<TG, MODE, 6, SET>();
+        case 7: return pick_tma_w<TG, MODE, 7, SET>();
+        case 8: return pick_tma_w<TG, MODE, 8, SET>();
+        default: return {nullptr, 0, 0, 0};
+    }
+}
+
+template <typename TG, bool SET = false>
 TmaLaunch pick_tma_t(int mode, int world) {
     switch (mode) {
-        case kMean: return pick_tma_m<TG, kMean>(world);
-        case kSgd: return pick_tma_m<TG, kSgd>(world);
-        case kSgdMp: return pick_tma_m<TG, kSgdMp>(world);
-        default: return {nullptr, 0, 0};
+        case kMean: return pick_tma_m<TG, kMean, SET>(world);
+        case kSgd: return pick_tma_m<TG, kSgd, SET>(world);
+        case kSgdMp: return pick_tma_m<TG, kSgdMp, SET>(world);
+        default: return {nullptr, 0, 0, 0};
     }
 }
 
@@ -1641,6 +1913,56 @@ bool use_tma_kernel(int dtype, int mode, int world) {
     return world >= 2;
 }
 
+// Opt a TMA kernel in to > 48 KiB of dynamic shared memory (once per device and kernel)
+// and return its co-resident CTAs per SM.
+static cudaError_t tma_prepare(const TmaLaunch &l, int dev, int *per_sm) {
+    static std::mutex mu;
+    static std::map<std::pair<int, void *>, int> occ;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_pair(dev, reinterpret_cast<void *>(l.fn));
+    auto it = occ.find(key);
+    if (it == occ.end()) {
+        cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(l.fn),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
+        if (e != cudaSuccess) return e;
+        int n = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, l.fn, l.threads, l.smem);
+        if (e != cudaSuccess) return e;
+        it = occ.emplace(key, n).first;
+    }
+    *per_sm = it->second;
+    return cudaSuccess;
+}
+
+cudaError_t launch_gdraa_tma_set(const KParams &p, int dtype, int mode, int vr_rows,
+                                 bool cooperative, cudaStream_t s, int ctas) {
+    TmaLaunch l = dtype == GDRAA_F32 ? pick_tma_t<float, true>(mode, p.world)
+                                     : pick_tma_t<__nv_bfloat16, true>(mode, p.world);
+    if (l.fn == nullptr) return cudaErrorInvalidValue;
+    int dev = 0, per_sm = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    e = tma_prepare(l, dev, &per_sm);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    int cap = sms * per_sm / vr_rows;
+    if (ctas > 0 && ctas < cap) cap = ctas;
+    if (cap < 1) return cudaErrorInvalidConfiguration;
+    dim3 grid(cap, vr_rows), block(l.threads);
+    if (cooperative) {
+        void *args[] = {const_cast<KParams *>(&p)};
+        return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(l.fn), grid, block,
+                                           args, l.smem, s);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = l.smem;
+    cfg.stream = s;
+    return cudaLaunchKernelEx(&cfg, l.fn, p);
+}
+
 cudaError_t launch_gdraa_tma(const KParams &p, int dtype, int mode, int vr_rows,
                              bool cooperative, cudaStream_t s, int *grid_x_out) {
     TmaLaunch l = dtype == GDRAA_F32 ? pick_tma_t<float>(mode, p.world)
@@ -1649,25 +1971,9 @@ cudaError_t launch_gdraa_tma(const KParams &p, int dtype, int mode, int vr_rows,
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    // opt in to > 48 KiB of dynamic shared memory once per (device, kernel)
-    static std::mutex mu;
-    static std::set<std::pair<int, void *>> ready;
-    static std::map<std::pair<int, void *>, int> occ;
     int per_sm = 0, sms = 0;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        const auto key = std::make_pair(dev, reinterpret_cast<void *>(l.fn));
-        if (!ready.count(key)) {
-            e = cudaFuncSetAttribute(reinterpret_cast<const void *>(l.fn),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
-            if (e != cudaSuccess) return e;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l.fn, l.threads, l.smem);
-            if (e != cudaSuccess) return e;
-            ready.insert(key);
-            occ[key] = per_sm;
-        }
-        per_sm = occ[key];
-    }
+    e = tma_prepare(l, dev, &per_sm);
+    if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
     int cap = sms * per_sm / vr_rows;

@@ -140,10 +140,84 @@ struct StreamOrder {
 // A bucket set (gdraa_bucket_set_begin / _end): the calls inside it skip their exit
 // barrier, so their results are complete only at _end; they must therefore write disjoint
 // destination ranges.  spans = the [lo, hi) byte ranges written so far in the open set.
+// A streamed set (gdraa_bucket_set_begin_streamed) is served by one persistent kernel on
+// the library's own stream, launched at the set's first call; every call then only
+// describes its bucket with stream memory operations on the caller's stream (SetDesc).
+struct Streamed {
+    bool on = false;                 // the open set is streamed
+    bool launched = false;           // its kernel has been launched (at the first call)
+    int ctas = 0;                    // CTAs per rank of that kernel
+    uint32_t gen = 0;                // set generation (tags in SetDesc)
+    uint32_t nb = 0;                 // buckets described so far
+    int mode = -1, dtype = -1;       // what the kernel was launched for
+    const void *key[4] = {};         // base pointers it was launched with: g, dst, v, wm
+    float lr = 0.f, mom = 0.f, wd = 0.f;
+    cudaStream_t last = nullptr;     // stream of the last described bucket
+    SetDesc *desc = nullptr;         // device memory
+    uint32_t *next = nullptr;        // device memory, kSetMax chunk counters per (v)rank
+    cudaStream_t ps = nullptr;       // the kernel's stream (non-blocking)
+    cudaEvent_t done = nullptr;      // recorded on ps after the kernel
+};
+
 struct BucketSet {
     bool open = false;
     std::vector<std::pair<uintptr_t, uintptr_t>> spans;
+    Streamed st;
 };
+
+// cuStreamWriteValue64 through the runtime's driver entry point (no -lcuda needed).
+using WriteValue64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+WriteValue64Fn write_value64_fn() {
+    static WriteValue64Fn fn = nullptr;
+    if (fn == nullptr) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<WriteValue64Fn>(p);
+    }
+    return fn;
+}
+
+int write_value(cudaStream_t s, const uint64_t *addr, uint64_t v) {
+    WriteValue64Fn wv = write_value64_fn();
+    if (wv == nullptr) return fail(GDRAA_ECUDA, "cuStreamWriteValue64 unavailable");
+    if (wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v, 0) != CUDA_SUCCESS)
+        return fail(GDRAA_ECUDA, "cuStreamWriteValue64 failed");
+    return GDRAA_OK;
+}
+
+// Open a streamed set: device state allocated on first use (rows = virtual ranks).
+int streamed_open(Streamed &st, int rows, int ctas) {
+    if (st.desc == nullptr) {
+        void *d = nullptr, *n = nullptr;
+        CUDA_TRY(cudaMalloc(&d, sizeof(SetDesc)));
+        CUDA_TRY(cudaMemset(d, 0, sizeof(SetDesc)));
+        CUDA_TRY(cudaMalloc(&n, sizeof(uint32_t) * kSetMax * rows));
+        CUDA_TRY(cudaMemset(n, 0, sizeof(uint32_t) * kSetMax * rows));
+        CUDA_TRY(cudaStreamCreateWithFlags(&st.ps, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming));
+        CUDA_TRY(cudaDeviceSynchronize());
+        st.desc = static_cast<SetDesc *>(d);
+        st.next = static_cast<uint32_t *>(n);
+    }
+    st.on = true;
+    st.launched = false;
+    st.ctas = ctas;
+    st.gen += 1;
+    st.nb = 0;
+    st.last = nullptr;
+    return GDRAA_OK;
+}
+
+void streamed_free(Streamed &st) {
+    if (st.desc) cudaFree(st.desc);
+    if (st.next) cudaFree(st.next);
+    if (st.ps) cudaStreamDestroy(st.ps);
+    if (st.done) cudaEventDestroy(st.done);
+    st = Streamed{};
+}
 
 int set_check(const BucketSet &b, const void *dst, size_t bytes) {
     if (!b.open) return GDRAA_OK;
@@ -419,6 +493,75 @@ int note_launch(StreamOrder &o, cudaStream_t s) {
     return GDRAA_OK;
 }
 
+// One call of an open streamed set.  p describes the call as for the per-call kernels
+// (pointers offset to the range's start); they are rebased to the buffers' starts, which
+// the persistent kernel indexes with each bucket's `first`.  The first call launches the
+// kernel on the set's own stream (ordered after the previous collective); every call then
+// describes its bucket on the caller's stream cs.
+int streamed_call(BucketSet &set, StreamOrder &order, KParams p, int rows, bool coop,
+                  int dtype, int mode, cudaStream_t cs, uint64_t first, uint64_t count) {
+    Streamed &st = set.st;
+    if (st.nb >= static_cast<uint32_t>(kSetMax) - 1)
+        return fail(GDRAA_EINVAL, "streamed bucket set: at most %d buckets", kSetMax - 1);
+    const size_t eg = elem_size(dtype), ed = mode == kSgd ? 4 : (mode == kSgdMp ? 2 : eg);
+    auto back = [&](const void *ptr, size_t es) -> void * {
+        return ptr == nullptr ? nullptr
+                              : const_cast<char *>(static_cast<const char *>(ptr)) - first * es;
+    };
+    for (int r = 0; r < rows; ++r) {
+        for (int q = 0; q < p.world; ++q) {
+            p.src[r][q] = back(p.src[r][q], eg);
+            p.dst[r][q] = back(p.dst[r][q], ed);
+        }
+        p.v[r] = static_cast<float *>(back(p.v[r], 4));
+        p.wm[r] = static_cast<float *>(back(p.wm[r], 4));
+    }
+    const void *key[4] = {p.src[0][p.rank0], p.dst[0][p.rank0], p.v[0], p.wm[0]};
+    if (!st.launched) {
+        p.sdesc = st.desc;
+        for (int r = 0; r < rows; ++r) p.snext[r] = st.next + static_cast<size_t>(r) * kSetMax;
+        p.sgen = st.gen;
+        int rc = order_after_previous(order, st.ps);
+        if (rc) return rc;
+        cudaError_t e = launch_gdraa_tma_set(p, dtype, mode, rows, coop, st.ps, st.ctas);
+        if (e != cudaSuccess)
+            return fail(GDRAA_ECUDA, "bucket-set kernel launch: %s", cudaGetErrorString(e));
+        CUDA_TRY(cudaEventRecord(st.done, st.ps));
+        note_launch(order, st.ps);
+        st.launched = true;
+        st.mode = mode;
+        st.dtype = dtype;
+        std::memcpy(st.key, key, sizeof key);
+        st.lr = p.lr;
+        st.mom = p.mom;
+        st.wd = p.wd;
+    } else if (mode != st.mode || dtype != st.dtype || std::memcmp(key, st.key, sizeof key) != 0 ||
+               p.lr != st.lr || p.mom != st.mom || p.wd != st.wd) {
+        return fail(GDRAA_EINVAL, "streamed bucket set: every call must use the buffers, mode, "
+                    "dtype and lr/mom/wd of the set's first call");
+    }
+    const uint32_t k = st.nb;
+    int rc = write_value(cs, &st.desc->first[k], first);
+    if (!rc) rc = write_value(cs, &st.desc->count[k], count);
+    if (!rc) rc = write_value(cs, &st.desc->ready[k], set_tag(st.gen, k));
+    if (rc) return rc;
+    st.nb += 1;
+    st.last = cs;
+    return GDRAA_OK;
+}
+
+// Close an open streamed set on s: the close marker, then s waits for the kernel.
+int streamed_close(BucketSet &set, StreamOrder &order, cudaStream_t s) {
+    Streamed &st = set.st;
+    st.on = false;
+    if (!st.launched) return GDRAA_OK;
+    st.launched = false;
+    int rc = write_value(s, &st.desc->ready[st.nb], set_close(st.gen));
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamWaitEvent(s, st.done, 0));
+    return note_launch(order, s);
+}
+
 int launch(const KParams &p, int dtype, int mode, cudaStream_t s) {
     int gx = 0;
     cudaError_t e = use_tma_kernel(dtype, mode, p.world)
@@ -525,6 +668,7 @@ struct VrArgs {
     int dtype;
     float lr, mom, wd;
     int mode;
+    size_t first = 0;    // element offset already applied to the pointers (range calls)
 };
 
 int vr_run(const VrArgs &a, cudaStream_t s) {
@@ -584,6 +728,12 @@ int vr_run(const VrArgs &a, cudaStream_t s) {
     for (int q = 0; q < world; ++q) {
         rc = set_check(set, dst[q], n * ed);
         if (rc) return rc;
+    }
+    if (set.open && set.st.on && world > 1) {          // streamed bucket set
+        rc = streamed_call(set, d->order, p, world, true, dtype, mode, s, a.first, n);
+        if (rc) return rc;
+        for (int q = 0; q < world; ++q) set_note(set, dst[q], n * ed);
+        return GDRAA_OK;
     }
     rc = order_after_previous(d->order, s);
     if (rc) return rc;
@@ -664,6 +814,7 @@ static void release_resources() {
     if (g.page) munmap(g.page, 4096);
     if (g.err_h) cudaFreeHost(g.err_h);
     if (g.order.ev) cudaEventDestroy(g.order.ev);
+    streamed_free(g.set.st);
     State s;
     g = s;
 }
@@ -882,6 +1033,13 @@ static int mean_common(void *buf, size_t first, size_t count, gdraa_stream_t s) 
         p.dst[0][q] = offset_ptr(r->peer[q], first, es);
     }
     const cudaStream_t cs = reinterpret_cast<cudaStream_t>(s);
+    if (g.set.open && g.set.st.on && g.world > 1) {    // streamed bucket set
+        rc = streamed_call(g.set, g.order, p, 1, false, r->dtype, kMean, cs, first, count);
+        if (rc) return rc;
+        account(count, r->dtype, 0);
+        set_note(g.set, offset_ptr(r->local, first, es), count * es);
+        return GDRAA_OK;
+    }
     rc = order_after_previous(g.order, cs);
     if (rc) return rc;
     if (g.ll != nullptr && count * es <= 8 * g.ll_pairs) {
@@ -949,6 +1107,13 @@ static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, 
     p.v[0] = static_cast<float *>(offset_ptr(v, first, 4));
     p.wm[0] = mode == kSgdMp ? static_cast<float *>(offset_ptr(wm, first, 4)) : nullptr;
     const cudaStream_t cs = reinterpret_cast<cudaStream_t>(s);
+    if (g.set.open && g.set.st.on && g.world > 1) {    // streamed bucket set
+        rc = streamed_call(g.set, g.order, p, 1, false, rg->dtype, mode, cs, first, count);
+        if (rc) return rc;
+        account(count, rg->dtype, mode == kSgd ? 4 : 2);
+        set_note(g.set, offset_ptr(rw->local, first, ew), count * ew);
+        return GDRAA_OK;
+    }
     rc = order_after_previous(g.order, cs);
     if (rc) return rc;
     if (g.ll != nullptr && count * eg <= g.ll_sgd_limit &&
@@ -1002,12 +1167,37 @@ int gdraa_bucket_set_begin(void) {
     return GDRAA_OK;
 }
 
+int gdraa_bucket_set_begin_streamed(int ctas) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.inited) return fail(GDRAA_ESTATE, "gdraa_init has not been called");
+    if (g.set.open) return fail(GDRAA_ESTATE, "a bucket set is already open");
+    if (ctas < 1) return fail(GDRAA_EINVAL, "ctas must be >= 1");
+    if (g.gated)
+        return fail(GDRAA_ESTATE, "streamed bucket sets need ungated mode (IterDone is "
+                    "written once per set)");
+    int rc = check_sticky();
+    if (rc) return rc;
+    if (g.world > 1) {
+        rc = streamed_open(g.set.st, 1, ctas);
+        if (rc) return rc;
+    }
+    g.set.open = true;
+    g.set.spans.clear();
+    return GDRAA_OK;
+}
+
 int gdraa_bucket_set_end(gdraa_stream_t s) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g.inited) return fail(GDRAA_ESTATE, "gdraa_init has not been called");
     if (!g.set.open) return fail(GDRAA_ESTATE, "no bucket set is open");
     g.set.open = false;
     g.set.spans.clear();
+    const cudaStream_t cs0 = reinterpret_cast<cudaStream_t>(s);
+    if (g.set.st.on) {                     // streamed: the kernel does the exit barrier
+        int rc = streamed_close(g.set, g.order, cs0);
+        if (rc) return rc;
+        return check_sticky();
+    }
     int rc = check_sticky();
     if (rc) return rc;
     if (g.world == 1) return GDRAA_OK;     // no barrier to defer
@@ -1033,6 +1223,9 @@ int gdraa_get_stats(gdraa_stats_t *out) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (out == nullptr) return fail(GDRAA_EINVAL, "null output");
     if (!g.inited) return fail(GDRAA_ESTATE, "gdraa_init has not been called");
+    if (g.set.st.launched)
+        return fail(GDRAA_ESTATE, "a streamed bucket set is open (its kernel waits for "
+                    "gdraa_bucket_set_end; synchronising now would wait for ever)");
     CUDA_TRY(cudaDeviceSynchronize());
     Pad host;
     CUDA_TRY(cudaMemcpy(&host, g.pad, sizeof host, cudaMemcpyDeviceToHost));
@@ -1049,6 +1242,12 @@ int gdraa_finalize(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g.inited) return fail(GDRAA_ESTATE, "gdraa_init has not been called");
     int rc = GDRAA_OK;
+    if (g.set.open && g.set.st.launched && !g.fatal) {
+        // a streamed set left open: close it where its last bucket was described
+        const int crc = streamed_close(g.set, g.order, g.set.st.last);
+        if (crc) rc = crc;
+        g.set.open = false;
+    }
     if (g.set.open && g.world > 1 && !g.fatal) {
         // a bucket set left open: run its deferred exit barrier so that the peers'
         // gdraa_bucket_set_end (which waits for ours) completes
@@ -1135,6 +1334,7 @@ static int vr_range(VrArgs a, size_t first, size_t count, cudaStream_t s) {
     a.v = a.v ? v : nullptr;
     a.wm = a.wm ? wm : nullptr;
     a.n = count;
+    a.first = first;
     return vr_run(a, s);
 }
 
@@ -1175,6 +1375,23 @@ int gdraa_vr_bucket_set_begin(int world) {
     return GDRAA_OK;
 }
 
+int gdraa_vr_bucket_set_begin_streamed(int world, int ctas) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (world < 1 || world > kMaxWorld) return fail(GDRAA_EINVAL, "world %d out of [1,%d]", world, kMaxWorld);
+    if (ctas < 1) return fail(GDRAA_EINVAL, "ctas must be >= 1");
+    VrDevice *d = nullptr;
+    int rc = vr_prepare(world, &d);
+    if (rc) return rc;
+    if (d->set[world].open) return fail(GDRAA_ESTATE, "a bucket set is already open (world %d)", world);
+    if (world > 1) {
+        rc = streamed_open(d->set[world].st, world, ctas);
+        if (rc) return rc;
+    }
+    d->set[world].open = true;
+    d->set[world].spans.clear();
+    return GDRAA_OK;
+}
+
 int gdraa_vr_bucket_set_end(int world, gdraa_stream_t s) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (world < 1 || world > kMaxWorld) return fail(GDRAA_EINVAL, "world %d out of [1,%d]", world, kMaxWorld);
@@ -1184,6 +1401,8 @@ int gdraa_vr_bucket_set_end(int world, gdraa_stream_t s) {
     if (!d->set[world].open) return fail(GDRAA_ESTATE, "no bucket set is open (world %d)", world);
     d->set[world].open = false;
     d->set[world].spans.clear();
+    if (d->set[world].st.on)
+        return streamed_close(d->set[world], d->order, reinterpret_cast<cudaStream_t>(s));
     if (world == 1) return GDRAA_OK;
     KParams p;
     std::memset(&p, 0, sizeof p);

@@ -30,7 +30,8 @@ EXPORTED = ["gdraa_sgd_step_ex", "gdraa_sgd_step_mp", "gdraa_poly_lr",
             "gdraa_version", "gdraa_vr_allreduce_mean", "gdraa_vr_sgd_step",
             "gdraa_vr_allreduce_mean_range", "gdraa_vr_sgd_step_range",
             "gdraa_vr_sgd_step_mp_range", "gdraa_bucket_set_begin", "gdraa_bucket_set_end",
-            "gdraa_vr_bucket_set_begin", "gdraa_vr_bucket_set_end"]
+            "gdraa_vr_bucket_set_begin", "gdraa_vr_bucket_set_end",
+            "gdraa_bucket_set_begin_streamed", "gdraa_vr_bucket_set_begin_streamed"]
 
 
 class GdraaError(RuntimeError):
@@ -90,6 +91,8 @@ _sig = {
     "gdraa_bucket_set_end": ([_vp], _i),
     "gdraa_vr_bucket_set_begin": ([_i], _i),
     "gdraa_vr_bucket_set_end": ([_i, _vp], _i),
+    "gdraa_bucket_set_begin_streamed": ([_i], _i),
+    "gdraa_vr_bucket_set_begin_streamed": ([_i, _i], _i),
 }
 for _name, (_args, _res) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -205,6 +208,10 @@ def gdraa_bucket_set_begin():
     _check(_lib.gdraa_bucket_set_begin(), "gdraa_bucket_set_begin")
 
 
+def gdraa_bucket_set_begin_streamed(ctas: int):
+    _check(_lib.gdraa_bucket_set_begin_streamed(ctas), "gdraa_bucket_set_begin_streamed")
+
+
 def gdraa_bucket_set_end(stream=None):
     _check(_lib.gdraa_bucket_set_end(_stream(stream)), "gdraa_bucket_set_end")
 
@@ -313,3 +320,8 @@ def gdraa_vr_bucket_set_begin(world: int):
 
 def gdraa_vr_bucket_set_end(world: int, stream=None):
     _check(_lib.gdraa_vr_bucket_set_end(world, _stream(stream)), "gdraa_vr_bucket_set_end")
+
+
+def gdraa_vr_bucket_set_begin_streamed(world: int, ctas: int):
+    _check(_lib.gdraa_vr_bucket_set_begin_streamed(world, ctas),
+           "gdraa_vr_bucket_set_begin_streamed")

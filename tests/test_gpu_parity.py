@@ -595,6 +595,92 @@ def test_vr_bucket_set(N, dt):
         compare(vmh[vmask], vm_exp[vmask], "f32", what=f"set mp v N={N} r{r}")
 
 
+@pytest.mark.parametrize("N", [2, 3, 4, 8])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("ctas", [4, 32])
+def test_vr_bucket_set_streamed(N, dt, ctas):
+    """Streamed bucket sets: one persistent kernel serves every bucket of the set (bucket
+    descriptions arrive by stream memory operations); out-of-order ragged buckets, one
+    of them smaller than the world; two chained sgd sets, then an mp set and a mean set --
+    the whole-buffer oracle's bits."""
+    bf16 = dt == "bf16"
+    L = 3_000_017
+    buckets = _buckets(L)
+    gs = make_grads("like", 960 + N, N, L, bf16)
+    w0, v0 = synth.w_like(960 + N, L), synth.w_like(970 + N, L)
+    wd, lr, mom = 0.001, synth.PAPER_LR, synth.PAPER_MOM
+    w1, v1 = oracle.sgd_step_wd(gs, w0, v0, lr, mom, wd)
+    w2, v2 = oracle.sgd_step_wd(gs, w1, v1, lr, mom, wd)
+    wm_exp, vm_exp, m_exp = oracle.sgd_step_wd(gs, w0, v0, lr, mom, wd, model_dtype=oracle.BF16)
+    g_d = [to_dev(g, bf16) for g in gs]
+    w_d = [to_dev(w0) for _ in range(N)]
+    v_d = [to_dev(v0) for _ in range(N)]
+    for it in range(2):
+        gdraa.gdraa_vr_bucket_set_begin_streamed(N, ctas)
+        for first, count in buckets:
+            gdraa.gdraa_vr_sgd_step_range(w_d, g_d, v_d, first, count, lr, mom, wd)
+        gdraa.gdraa_vr_bucket_set_end(N)
+        if it == 0:
+            torch.cuda.synchronize()
+            for r in range(N):
+                compare(from_dev(w_d[r]), w1, "f32", what=f"streamed w it0 N={N} r{r}")
+    wm_d = [to_dev(w0) for _ in range(N)]
+    vm_d = [to_dev(v0) for _ in range(N)]
+    model_d = [torch.zeros(L, dtype=torch.bfloat16, device=DEV) for _ in range(N)]
+    gdraa.gdraa_vr_bucket_set_begin_streamed(N, ctas)
+    for first, count in buckets:
+        gdraa.gdraa_vr_sgd_step_mp_range(wm_d, model_d, g_d, vm_d, first, count, lr, mom, wd)
+    gdraa.gdraa_vr_bucket_set_end(N)
+    bufs = [to_dev(g, bf16) for g in gs]
+    gdraa.gdraa_vr_bucket_set_begin_streamed(N, ctas)
+    for first, count in buckets:
+        gdraa.gdraa_vr_allreduce_mean_range(bufs, first, count)
+    gdraa.gdraa_vr_bucket_set_end(N)
+    torch.cuda.synchronize()
+    mean_exp = oracle.allreduce_mean(gs)
+    for r in range(N):
+        compare(from_dev(w_d[r]), w2, "f32", what=f"streamed w it1 N={N} r{r}")
+        compare(from_dev(model_d[r]), m_exp, "bf16", what=f"streamed mp model N={N} r{r}")
+        compare(from_dev(bufs[r]), mean_exp, dt, what=f"streamed mean N={N} r{r}")
+        vh, wmh, vmh, vmask = from_dev(v_d[r]), from_dev(wm_d[r]), from_dev(vm_d[r]), np.zeros(L, bool)
+        for first, count in buckets:
+            off, ln = gdraa.gdraa_shard(N, r, count)
+            vmask[first + off:first + off + ln] = True
+        compare(vh[vmask], v2[vmask], "f32", what=f"streamed v N={N} r{r}")
+        compare(wmh[vmask], wm_exp[vmask], "f32", what=f"streamed mp master N={N} r{r}")
+        compare(vmh[vmask], vm_exp[vmask], "f32", what=f"streamed mp v N={N} r{r}")
+        assert np.array_equal(vh[~vmask].view(np.uint32), v0[~vmask].view(np.uint32))
+
+
+def test_vr_bucket_set_streamed_rules():
+    """A streamed set serves one buffer set, mode and hyper-parameter set."""
+    N, L = 2, 1 << 16
+    w = [torch.zeros(L, device=DEV) for _ in range(N)]
+    w2 = [torch.zeros(L, device=DEV) for _ in range(N)]
+    g = [torch.ones(L, device=DEV) for _ in range(N)]
+    v = [torch.zeros(L, device=DEV) for _ in range(N)]
+    with pytest.raises(gdraa.GdraaError) as e:
+        gdraa.gdraa_vr_bucket_set_begin_streamed(N, 0)
+    assert e.value.name == "GDRAA_EINVAL"
+    gdraa.gdraa_vr_bucket_set_begin_streamed(N, 8)
+    gdraa.gdraa_vr_sgd_step_range(w, g, v, 0, 1024, 0.5, 0.0)
+    for call in (lambda: gdraa.gdraa_vr_sgd_step_range(w, g, v, 1024, 1024, 0.25, 0.0),  # lr
+                 lambda: gdraa.gdraa_vr_sgd_step_range(w2, g, v, 1024, 1024, 0.5, 0.0),  # w
+                 lambda: gdraa.gdraa_vr_allreduce_mean_range(w, 1024, 1024)):             # mode
+        with pytest.raises(gdraa.GdraaError) as e:
+            call()
+        assert e.value.name == "GDRAA_EINVAL"
+    gdraa.gdraa_vr_sgd_step_range(w, g, v, 1024, L - 1024, 0.5, 0.0)
+    gdraa.gdraa_vr_bucket_set_end(N)
+    torch.cuda.synchronize()
+    for r in range(N):
+        assert torch.equal(w[r], torch.full((L,), -0.5, device=DEV))
+    # an empty streamed set launches nothing and closes cleanly
+    gdraa.gdraa_vr_bucket_set_begin_streamed(N, 8)
+    gdraa.gdraa_vr_bucket_set_end(N)
+    torch.cuda.synchronize()
+
+
 def test_vr_bucket_set_rules():
     """Set state errors and the disjoint-destination rule inside a set."""
     N, L = 2, 1 << 16

@@ -286,6 +286,30 @@ def _bucket_worker(rank, world, sock, out_dir):
         st1 = gdraa.gdraa_get_stats()
         # per set: one entry barrier per two-shot bucket + the set's single exit barrier
         assert st1["sync_waits"] - st0["sync_waits"] == 2 * (two_shot + 1), (st0, st1)
+        # the same two iterations as streamed sets (one persistent kernel per set)
+        w.copy_(torch.from_numpy(w0).to(dev))
+        v.copy_(torch.from_numpy(v0).to(dev))
+        for it in range(2):
+            gdraa.gdraa_bucket_set_begin_streamed(16)
+            for first, count in set_buckets:
+                done = torch.cuda.Event()
+                done.record(torch.cuda.current_stream())
+                side.wait_event(done)
+                gdraa.gdraa_sgd_step_range(w, g, v, first, count, 0.1, 0.9, 0.001, stream=side)
+            gdraa.gdraa_bucket_set_end(stream=side)
+            torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        compare(from_dev(w), w2, "f32", what=f"streamed set w {dt} r{rank}")
+        vh = from_dev(v)
+        for first, count in set_buckets:
+            off, ln = gdraa.gdraa_shard(world, rank, count)
+            a, b = first + off, first + off + ln
+            compare(vh[a:b], v2[a:b], "f32", what=f"streamed set v {dt} r{rank}")
+        st2 = gdraa.gdraa_get_stats()
+        n_b = len(set_buckets)
+        assert st2["calls"] - st1["calls"] == 2 * n_b, (st1, st2)
+        assert st2["sync_waits"] - st1["sync_waits"] == 2 * (n_b + 1), (st1, st2)
+        assert st2["iter_done"] == st2["calls"], st2
         for t in (w, g):
             gdraa.gdraa_deregister(t)
     gdraa.gdraa_finalize()

@@ -31,6 +31,9 @@ def main():
     ap.add_argument("--set", action="store_true",
                     help="issue the buckets of one iteration as a bucket set "
                          "(gdraa_bucket_set_begin/_end: one deferred exit barrier per set)")
+    ap.add_argument("--streamed", type=int, default=0, metavar="CTAS",
+                    help="issue the buckets as a STREAMED bucket set: one persistent kernel "
+                         "of CTAS CTAs per rank serves all of them")
     args = ap.parse_args()
     out = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
@@ -108,24 +111,30 @@ def main():
 
     evs = [torch.cuda.Event() for _ in range(K)]
 
-    def overlap():
-        if args.set:
+    def set_begin():
+        if args.streamed:
+            gdraa.gdraa_bucket_set_begin_streamed(args.streamed)
+        elif args.set:
             gdraa.gdraa_bucket_set_begin()
+
+    in_set = args.set or args.streamed > 0
+
+    def overlap():
+        set_begin()
         for k, (first, count) in enumerate(buckets):
             torch.mm(A, A, out=C)               # "produces" bucket k
             evs[k].record(main_s)
             side.wait_event(evs[k])
             gdraa.gdraa_sgd_step_range(w, g, v, first, count, lr, mom, 0.0, stream=side)
-        if args.set:
+        if in_set:
             gdraa.gdraa_bucket_set_end(stream=side)
         main_s.wait_stream(side)
 
     def comm_buckets():
-        if args.set:
-            gdraa.gdraa_bucket_set_begin()
+        set_begin()
         for first, count in buckets:
             gdraa.gdraa_sgd_step_range(w, g, v, first, count, lr, mom, 0.0)
-        if args.set:
+        if in_set:
             gdraa.gdraa_bucket_set_end()
 
     t_bwd = timed(bwd, args.iters)
@@ -136,7 +145,8 @@ def main():
         hidden = (t_serial - t_overlap) / min(t_bwd, t_comm)
         line = {"n_gpus": world, "L": L, "buckets": K, "gemm_n": n,
                 "max_ctas": os.environ.get("GDRAA_MAX_CTAS", "all"),
-                "kernel": os.environ.get("GDRAA_KERNEL", "default"), "bucket_set": args.set,
+                "kernel": os.environ.get("GDRAA_KERNEL", "default"), "bucket_set": "streamed" if args.streamed else args.set,
+                "streamed_ctas": args.streamed,
                 "bwd_us": t_bwd * 1e3, "comm_us": t_comm * 1e3,
                 "comm_bucketed_us": t_comm_b * 1e3, "serial_us": t_serial * 1e3,
                 "overlap_us": t_overlap * 1e3, "speedup": t_serial / t_overlap,
