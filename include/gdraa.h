@@ -223,7 +223,9 @@ int gdraa_bucket_set_end(gdraa_stream_t s);
  * gdraa_bucket_set_begin (results complete at gdraa_bucket_set_end, disjoint destination
  * ranges), served by ONE persistent kernel instead of one kernel per call.  The set's
  * first call launches that kernel, with `ctas` CTAs per rank, on a stream of the
- * library's own (ordered after the previous collective); each call then only describes
+ * library's own, ordered after the previous collective and after the first call's
+ * stream reaches the call (so it holds no SMs before the first bucket is final); each
+ * call then only describes
  * its bucket with three stream memory operations (cuStreamWriteValue64) on the caller's
  * stream, which take effect when that stream reaches the call -- i.e. when the bucket's
  * gradient is final -- and the kernel reduces, updates and broadcasts each bucket as its

@@ -157,6 +157,7 @@ struct Streamed {
     uint32_t *next = nullptr;        // device memory, kSetMax chunk counters per (v)rank
     cudaStream_t ps = nullptr;       // the kernel's stream (non-blocking)
     cudaEvent_t done = nullptr;      // recorded on ps after the kernel
+    cudaEvent_t start = nullptr;     // the first call's stream, when it reaches that call
 };
 
 struct BucketSet {
@@ -198,6 +199,7 @@ int streamed_open(Streamed &st, int rows, int ctas) {
         CUDA_TRY(cudaMemset(n, 0, sizeof(uint32_t) * kSetMax * rows));
         CUDA_TRY(cudaStreamCreateWithFlags(&st.ps, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&st.start, cudaEventDisableTiming));
         CUDA_TRY(cudaDeviceSynchronize());
         st.desc = static_cast<SetDesc *>(d);
         st.next = static_cast<uint32_t *>(n);
@@ -216,6 +218,7 @@ void streamed_free(Streamed &st) {
     if (st.next) cudaFree(st.next);
     if (st.ps) cudaStreamDestroy(st.ps);
     if (st.done) cudaEventDestroy(st.done);
+    if (st.start) cudaEventDestroy(st.start);
     st = Streamed{};
 }
 
@@ -523,6 +526,10 @@ int streamed_call(BucketSet &set, StreamOrder &order, KParams p, int rows, bool 
         p.sgen = st.gen;
         int rc = order_after_previous(order, st.ps);
         if (rc) return rc;
+        // the kernel becomes resident (and holds its SMs) only once the first bucket is
+        // final, i.e. when the caller's stream reaches this call
+        CUDA_TRY(cudaEventRecord(st.start, cs));
+        CUDA_TRY(cudaStreamWaitEvent(st.ps, st.start, 0));
         cudaError_t e = launch_gdraa_tma_set(p, dtype, mode, rows, coop, st.ps, st.ctas);
         if (e != cudaSuccess)
             return fail(GDRAA_ECUDA, "bucket-set kernel launch: %s", cudaGetErrorString(e));

@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--set", action="store_true",
                     help="issue the buckets of one iteration as a bucket set "
                          "(gdraa_bucket_set_begin/_end: one deferred exit barrier per set)")
+    ap.add_argument("--comm-only", action="store_true",
+                    help="time only the whole-buffer and the bucketed step (no backward)")
     ap.add_argument("--streamed", type=int, default=0, metavar="CTAS",
                     help="issue the buckets as a STREAMED bucket set: one persistent kernel "
                          "of CTAS CTAs per rank serves all of them")
@@ -137,10 +139,13 @@ def main():
         if in_set:
             gdraa.gdraa_bucket_set_end()
 
-    t_bwd = timed(bwd, args.iters)
     t_comm_b = timed(comm_buckets, args.iters)
-    t_serial = timed(serial, args.iters)
-    t_overlap = timed(overlap, args.iters)
+    if args.comm_only:
+        t_bwd = t_serial = t_overlap = float("nan")
+    else:
+        t_bwd = timed(bwd, args.iters)
+        t_serial = timed(serial, args.iters)
+        t_overlap = timed(overlap, args.iters)
     if rank == 0:
         hidden = (t_serial - t_overlap) / min(t_bwd, t_comm)
         line = {"n_gpus": world, "L": L, "buckets": K, "gemm_n": n,
