@@ -1485,10 +1485,9 @@ gdraa_tma_set_kernel(const __grid_constant__ KParams p) {
             const uint64_t first = s_first[s];
             const Geo g = geo(s_count[s]);
             if (c == g.nchunks) {
-                if (ct < C::CW * 32)
-                    tail_scalar<TG, WORLD, MODE>(p, vr, rank, first + g.off + g.lenv + ct,
-                                                 first + g.off + g.len, C::CW * 32, vloc, wloc,
-                                                 p.lr, p.mom, p.wd);
+                tail_scalar<TG, WORLD, MODE>(p, vr, rank, first + g.off + g.lenv + ct,
+                                             first + g.off + g.len, C::CW * 32, vloc, wloc,
+                                             p.lr, p.mom, p.wd);
             } else {
                 uint64_t e0;
                 uint32_t n_el;
