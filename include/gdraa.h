@@ -242,7 +242,9 @@ int gdraa_bucket_set_end(gdraa_stream_t s);
  *  - nothing may wait for the set's completion before gdraa_bucket_set_end has been
  *    issued (the kernel is still waiting for buckets): no cudaDeviceSynchronize, no wait
  *    on the set's streams; gdraa_get_stats returns ESTATE while such a set is open;
- *  - not available in gated mode (ESTATE); world 1 behaves as gdraa_bucket_set_begin.
+ *  - not available in gated mode (ESTATE); world 1 behaves as gdraa_bucket_set_begin;
+ *  - not capturable into a CUDA graph (the kernel runs on the library's own stream);
+ *  - gdraa_finalize with such a set open closes it on the stream of its last call.
  * Errors: ESTATE (not initialised, set already open, gated), EINVAL (ctas < 1), ECUDA.
  */
 int gdraa_bucket_set_begin_streamed(int ctas);
