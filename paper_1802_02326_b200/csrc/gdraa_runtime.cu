@@ -504,6 +504,8 @@ int note_launch(StreamOrder &o, cudaStream_t s) {
 int streamed_call(BucketSet &set, StreamOrder &order, KParams p, int rows, bool coop,
                   int dtype, int mode, cudaStream_t cs, uint64_t first, uint64_t count) {
     Streamed &st = set.st;
+    if (capturing(cs))
+        return fail(GDRAA_EINVAL, "streamed bucket sets cannot be captured into a CUDA graph");
     if (st.nb >= static_cast<uint32_t>(kSetMax) - 1)
         return fail(GDRAA_EINVAL, "streamed bucket set: at most %d buckets", kSetMax - 1);
     const size_t eg = elem_size(dtype), ed = mode == kSgd ? 4 : (mode == kSgdMp ? 2 : eg);
