@@ -652,6 +652,48 @@ def test_vr_bucket_set_streamed(N, dt, ctas):
         assert np.array_equal(vh[~vmask].view(np.uint32), v0[~vmask].view(np.uint32))
 
 
+@pytest.mark.parametrize("N", [1, 2, 4])
+@pytest.mark.parametrize("kind", ["set", "streamed"])
+def test_vr_bucket_sets_two_streams(N, kind):
+    """Bucket calls alternating between two streams inside one set (each bucket's stream
+    waits for an event that marks its gradient final), the set closed on a third: the
+    cross-stream ordering of the library makes it the whole-buffer oracle step.  N = 1:
+    both kinds degenerate to plain calls."""
+    L = 2_000_003
+    buckets = _buckets(L)
+    gs = make_grads("like", 990 + N, N, L, False)
+    w0, v0 = synth.w_like(990 + N, L), synth.w_like(995 + N, L)
+    w_exp, v_exp = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, 0.001)
+    g_d = [to_dev(g) for g in gs]
+    w_d = [to_dev(w0) for _ in range(N)]
+    v_d = [to_dev(v0) for _ in range(N)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    closer = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    if kind == "set":
+        gdraa.gdraa_vr_bucket_set_begin(N)
+    else:
+        gdraa.gdraa_vr_bucket_set_begin_streamed(N, 32)
+    for k, (first, count) in enumerate(buckets):
+        ev = torch.cuda.Event()
+        ev.record(main)
+        st = streams[k % 2]
+        st.wait_event(ev)
+        gdraa.gdraa_vr_sgd_step_range(w_d, g_d, v_d, first, count, 0.1, 0.9, 0.001, stream=st)
+    for st in streams:
+        closer.wait_stream(st)
+    gdraa.gdraa_vr_bucket_set_end(N, stream=closer)
+    main.wait_stream(closer)
+    torch.cuda.synchronize()
+    for r in range(N):
+        compare(from_dev(w_d[r]), w_exp, "f32", what=f"{kind} two streams w N={N} r{r}")
+        vh, vmask = from_dev(v_d[r]), np.zeros(L, bool)
+        for first, count in buckets:
+            off, ln = gdraa.gdraa_shard(N, r, count)
+            vmask[first + off:first + off + ln] = True
+        compare(vh[vmask], v_exp[vmask], "f32", what=f"{kind} two streams v N={N} r{r}")
+
+
 def test_vr_bucket_set_streamed_rules():
     """A streamed set serves one buffer set, mode and hyper-parameter set."""
     N, L = 2, 1 << 16
