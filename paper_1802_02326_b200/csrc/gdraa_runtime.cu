@@ -462,7 +462,7 @@ void fill_common(KParams &p, uint64_t n) {
 }
 
 // Lemma 1/2 accounting of one call (s_w: bytes per broadcast element; 0 = same as g).
-void account(uint64_t n, int dtype_g, uint64_t s_w) {
+void account(uint64_t n, int dtype_g, uint64_t s_w, bool launched = true) {
     uint64_t blk, off, len;
     partition(n, g.world, g.rank, &blk, &off, &len);
     const uint64_t sg = elem_size(dtype_g), sw = s_w ? s_w : sg, n1 = g.world - 1;
@@ -472,7 +472,7 @@ void account(uint64_t n, int dtype_g, uint64_t s_w) {
     g.host.ag_bytes_in += sw * (n - len);
     g.host.adds += n1 * len;
     g.host.divides += len;
-    g.host.launches += 1;
+    if (launched) g.host.launches += 1;
 }
 
 bool capturing(cudaStream_t s) {
@@ -1043,9 +1043,10 @@ static int mean_common(void *buf, size_t first, size_t count, gdraa_stream_t s) 
     }
     const cudaStream_t cs = reinterpret_cast<cudaStream_t>(s);
     if (g.set.open && g.set.st.on && g.world > 1) {    // streamed bucket set
+        const bool first_call = !g.set.st.launched;
         rc = streamed_call(g.set, g.order, p, 1, false, r->dtype, kMean, cs, first, count);
         if (rc) return rc;
-        account(count, r->dtype, 0);
+        account(count, r->dtype, 0, first_call);
         set_note(g.set, offset_ptr(r->local, first, es), count * es);
         return GDRAA_OK;
     }
@@ -1117,9 +1118,10 @@ static int sgd_common(int mode, float *wm, void *dst, const void *gr, float *v, 
     p.wm[0] = mode == kSgdMp ? static_cast<float *>(offset_ptr(wm, first, 4)) : nullptr;
     const cudaStream_t cs = reinterpret_cast<cudaStream_t>(s);
     if (g.set.open && g.set.st.on && g.world > 1) {    // streamed bucket set
+        const bool first_call = !g.set.st.launched;
         rc = streamed_call(g.set, g.order, p, 1, false, rg->dtype, mode, cs, first, count);
         if (rc) return rc;
-        account(count, rg->dtype, mode == kSgd ? 4 : 2);
+        account(count, rg->dtype, mode == kSgd ? 4 : 2, first_call);
         set_note(g.set, offset_ptr(rw->local, first, ew), count * ew);
         return GDRAA_OK;
     }
