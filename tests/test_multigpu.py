@@ -309,6 +309,7 @@ def _bucket_worker(rank, world, sock, out_dir):
         n_b = len(set_buckets)
         assert st2["calls"] - st1["calls"] == 2 * n_b, (st1, st2)
         assert st2["sync_waits"] - st1["sync_waits"] == 2 * (n_b + 1), (st1, st2)
+        assert st2["launches"] - st1["launches"] == 2, (st1, st2)     # one kernel per set
         assert st2["iter_done"] == st2["calls"], st2
         for t in (w, g):
             gdraa.gdraa_deregister(t)
