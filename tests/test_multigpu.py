@@ -550,6 +550,68 @@ def test_multiprocess_full_size_sampled(tmp_path):
         assert json.load(open(tmp_path / f"full{r}.json"))["checked"] > 0
 
 
+def _c5_worker(rank, world, sock, out_dir):
+    """Config 5 sizes through the multi-process path: allreduce_mean of fp32 buffers of
+    2^k bytes, k = 10..30 (the small-message kernel below its threshold, the two-shot
+    kernel above), against the oracle -- whole buffers up to 4 MiB, sampled windows at
+    every shard boundary, the ragged end, the all-ranks -0.0 segment and random places
+    above."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    import synth
+    from paper_1802_02326_b200 import gdraa
+    from tests._parity import compare
+    from tests.test_gpu_parity import from_dev, to_dev
+
+    from tests.conftest import rank_device
+    dev = rank_device(rank)
+    os.environ["GDRAA_JOBSERVER"] = sock
+    gdraa.gdraa_init(world, rank)
+    checked = 0
+    for k in range(10, 31):
+        L = (1 << k) // 4
+        seed = 500 + k
+        gh = synth.grad_like_full(seed, rank, L)
+        buf = to_dev(gh, dev=dev)
+        del gh
+        gdraa.gdraa_register(buf)
+        gdraa.gdraa_allreduce_mean(buf)
+        torch.cuda.synchronize()
+        if L <= (1 << 20):
+            gs = [synth.grad_like_full(seed, p, L) for p in range(world)]
+            compare(from_dev(buf), oracle.allreduce_mean(gs), "f32", what=f"c5 2^{k} B r{rank}")
+            checked += L
+        else:
+            for a in _windows(L, world, seed):
+                got = from_dev(buf[a:a + WIN])
+                compare(got, oracle.allreduce_mean(_window_grads(seed, world, a, L, False)),
+                        "f32", what=f"c5 2^{k} B @{a} r{rank}")
+                checked += WIN
+        gdraa.gdraa_deregister(buf)
+        del buf
+        torch.cuda.empty_cache()
+    gdraa.gdraa_finalize()
+    with open(os.path.join(out_dir, f"c5_{rank}.json"), "w") as f:
+        json.dump({"checked": checked}, f)
+
+
+def test_multiprocess_config5_sizes(tmp_path):
+    """Config 5 (allreduce message-size sweep 1 KiB - 1 GiB) bit-exact against the oracle
+    through the multi-process path at every size of the sweep."""
+    from paper_1802_02326_b200 import jobserver
+    world = mp_world()
+    sock = str(tmp_path / "js.sock")
+    js = jobserver.start(world, sock)
+    try:
+        mp.start_processes(_c5_worker, args=(world, sock, str(tmp_path)), nprocs=world,
+                           join=True, start_method="spawn")
+    finally:
+        js.communicate(timeout=300)
+    for r in range(world):
+        assert json.load(open(tmp_path / f"c5_{r}.json"))["checked"] > 0
+
+
 def test_multiprocess_config4_world8(tmp_path):
     """Config 4 as BASELINE.json states it -- ResNet-50 bf16 gradients, fp32 accumulation
     and master weights, 8 ranks -- at full size through the multi-process path (+ the
