@@ -10,7 +10,7 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU; run via gpurun")
-    config.addinivalue_line("markers", "multigpu: needs >= 2 GPUs on one box")
+    config.addinivalue_line("markers", "multigpu: multi-process path (one rank per GPU; time-sliced ranks on a one-GPU box)")
 
 
 def has_cuda():
