@@ -31,6 +31,10 @@ def main():
     ap.add_argument("--set", action="store_true",
                     help="issue the buckets of one iteration as a bucket set "
                          "(gdraa_bucket_set_begin/_end: one deferred exit barrier per set)")
+    ap.add_argument("--nccl", action="store_true",
+                    help="reference point: each bucket as torch.distributed all_reduce(AVG) "
+                         "(NCCL) followed by torch's momentum-SGD ops on the bucket, the "
+                         "DDP-plus-optimizer pattern, instead of the library")
     ap.add_argument("--comm-only", action="store_true",
                     help="time only the whole-buffer and the bucketed step (no backward)")
     ap.add_argument("--streamed", type=int, default=0, metavar="CTAS",
@@ -85,8 +89,24 @@ def main():
         torch.cuda.synchronize()
         return t_max(e0.elapsed_time(e1) / iters)
 
+    def nccl_step(first, count, stream):
+        with torch.cuda.stream(stream):
+            gb, vb, wb = g[first:first + count], v[first:first + count], w[first:first + count]
+            dist.all_reduce(gb, op=dist.ReduceOp.AVG)
+            vb.mul_(mom).add_(gb)
+            wb.add_(vb, alpha=-lr)
+
+    def step_range(first, count, stream):
+        if args.nccl:
+            nccl_step(first, count, stream)
+        else:
+            gdraa.gdraa_sgd_step_range(w, g, v, first, count, lr, mom, 0.0, stream=stream)
+
     def comm():
-        gdraa.gdraa_sgd_step(w, g, v, lr, mom)
+        if args.nccl:
+            nccl_step(0, L, main_s)
+        else:
+            gdraa.gdraa_sgd_step(w, g, v, lr, mom)
 
     t_comm = timed(comm, args.iters)
 
@@ -114,12 +134,14 @@ def main():
     evs = [torch.cuda.Event() for _ in range(K)]
 
     def set_begin():
+        if args.nccl:
+            return
         if args.streamed:
             gdraa.gdraa_bucket_set_begin_streamed(args.streamed)
         elif args.set:
             gdraa.gdraa_bucket_set_begin()
 
-    in_set = args.set or args.streamed > 0
+    in_set = (args.set or args.streamed > 0) and not args.nccl
 
     def overlap():
         set_begin()
@@ -127,7 +149,7 @@ def main():
             torch.mm(A, A, out=C)               # "produces" bucket k
             evs[k].record(main_s)
             side.wait_event(evs[k])
-            gdraa.gdraa_sgd_step_range(w, g, v, first, count, lr, mom, 0.0, stream=side)
+            step_range(first, count, side)
         if in_set:
             gdraa.gdraa_bucket_set_end(stream=side)
         main_s.wait_stream(side)
@@ -135,7 +157,7 @@ def main():
     def comm_buckets():
         set_begin()
         for first, count in buckets:
-            gdraa.gdraa_sgd_step_range(w, g, v, first, count, lr, mom, 0.0)
+            step_range(first, count, main_s)
         if in_set:
             gdraa.gdraa_bucket_set_end()
 
@@ -151,7 +173,7 @@ def main():
         line = {"n_gpus": world, "L": L, "buckets": K, "gemm_n": n,
                 "max_ctas": os.environ.get("GDRAA_MAX_CTAS", "all"),
                 "kernel": os.environ.get("GDRAA_KERNEL", "default"), "bucket_set": "streamed" if args.streamed else args.set,
-                "streamed_ctas": args.streamed,
+                "streamed_ctas": args.streamed, "impl": "nccl+torch" if args.nccl else "gdraa",
                 "bwd_us": t_bwd * 1e3, "comm_us": t_comm * 1e3,
                 "comm_bucketed_us": t_comm_b * 1e3, "serial_us": t_serial * 1e3,
                 "overlap_us": t_overlap * 1e3, "speedup": t_serial / t_overlap,
