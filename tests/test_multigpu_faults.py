@@ -38,11 +38,18 @@ def _setup(rank, world, sock, timeout_ms, n):
 def _timeout_worker(rank, world, sock, out, mode, n):
     # rank 0 gives up after 1.5 s when the peer just skips the call; when the peer dies
     # it keeps a 60 s timeout, so only the job server's abort flag can end its wait early
-    gdraa, w, g, v = _setup(rank, world, sock, 1500 if rank == 0 and mode == "skip" else 60000, n)
+    gdraa, w, g, v = _setup(rank, world, sock,
+                            1500 if rank == 0 and mode in ("skip", "streamed") else 60000, n)
     res = {"rank": rank}
     if rank == 0:
         t0 = time.time()
-        gdraa.gdraa_sgd_step(w, g, v, 0.1, 0.9)        # the peer never arrives
+        if mode == "streamed":
+            # one bucket of a streamed set: the persistent kernel's entry wait gives up
+            gdraa.gdraa_bucket_set_begin_streamed(8)
+            gdraa.gdraa_sgd_step_range(w, g, v, 0, n, 0.1, 0.9)
+            gdraa.gdraa_bucket_set_end()
+        else:
+            gdraa.gdraa_sgd_step(w, g, v, 0.1, 0.9)    # the peer never arrives
         torch.cuda.synchronize()                         # kernel gives up after 1.5 s
         res["kernel_s"] = time.time() - t0
         try:
@@ -91,6 +98,16 @@ SIZES = [1 << 18, 1 << 21]
 @pytest.mark.parametrize("n", SIZES)
 def test_peer_timeout_names_missing_rank(tmp_path, n):
     codes, r0, _ = _run(tmp_path, "skip", n)
+    assert codes == [0, 0], codes
+    assert 1.0 < r0["kernel_s"] < 20, r0
+    assert r0["second"] == "GDRAA_ETIMEOUT" and "missing rank(s) 1" in r0["msg"], r0
+    assert r0["finalize"] == "GDRAA_ETIMEOUT", r0
+
+
+def test_streamed_set_peer_timeout(tmp_path):
+    """The persistent bucket-set kernel gives up like the per-call kernels: the set ends,
+    the next call reports GDRAA_ETIMEOUT naming the missing rank."""
+    codes, r0, _ = _run(tmp_path, "streamed", 1 << 21)
     assert codes == [0, 0], codes
     assert 1.0 < r0["kernel_s"] < 20, r0
     assert r0["second"] == "GDRAA_ETIMEOUT" and "missing rank(s) 1" in r0["msg"], r0
