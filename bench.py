@@ -356,12 +356,22 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun")
+    # GDRAA_BENCH_OVERSUBSCRIBE=1: a functional check of the N-rank path on a box with
+    # fewer GPUs (ranks share GPUs round-robin, time-sliced; gloo plumbing, no NCCL
+    # reference).  Its times are meaningless and the JSON line says so.
+    oversub = os.environ.get("GDRAA_BENCH_OVERSUBSCRIBE") == "1"
+    if oversub:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     js = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        js = jobserver.setup_for_rank(world, rank, local)
+        if oversub:
+            dist.init_process_group("gloo")
+            args.no_nccl = True
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+        js = jobserver.setup_for_rank(world, rank, int(os.environ.get("LOCAL_RANK", "0")))
     gdraa.gdraa_init(world, rank)
 
     L, g_dt, desc = CONFIGS[args.config]
@@ -419,7 +429,7 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier() if oversub else dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
     for k in range(args.warmup):
@@ -663,6 +673,10 @@ def main():
             "gpu_launches": launches, "clocks": clocks.summary() if clocks else None,
             "nccl_reference": nccl,
         }
+        if oversub:
+            line["oversubscribed"] = ("functional check only: %d ranks time-sliced on %d GPUs; "
+                                      "the times are not a measurement"
+                                      % (N, torch.cuda.device_count()))
         print(json.dumps(line), file=OUT, flush=True)
 
     barrier()
