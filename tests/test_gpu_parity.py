@@ -420,6 +420,51 @@ def test_graph_capture_replays():
         compare(from_dev(w_d[r]), w_ref, "f32", what=f"graph w rank {r}")
 
 
+@pytest.mark.parametrize("N", [2, 4])
+def test_graph_capture_bucket_set(N):
+    """A bucket set (per-call kernels with the deferred exit, and the exit kernel)
+    captured once into a CUDA graph and replayed as three chained iterations; a streamed
+    set refuses capture (EINVAL)."""
+    L = 1_500_007
+    buckets = _buckets(L)
+    gs = make_grads("like", 31 + N, N, L, False)
+    w0, v0 = synth.w_like(31 + N, L), synth.w_like(32 + N, L)
+    g_d = [to_dev(g) for g in gs]
+    w_d = [to_dev(w0) for _ in range(N)]
+    v_d = [to_dev(v0) for _ in range(N)]
+    s = torch.cuda.Stream()
+
+    def one_iteration():
+        gdraa.gdraa_vr_bucket_set_begin(N)
+        for first, count in buckets:
+            gdraa.gdraa_vr_sgd_step_range(w_d, g_d, v_d, first, count, 0.1, 0.9, 0.001, stream=s)
+        gdraa.gdraa_vr_bucket_set_end(N, stream=s)
+
+    w_ref, v_ref = oracle.sgd_step_wd(gs, w0, v0, 0.1, 0.9, 0.001)
+    one_iteration()                                   # warm up (pads, LL slots allocated)
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        one_iteration()
+    for _ in range(3):
+        graph.replay()
+        w_ref, v_ref = oracle.sgd_step_wd(gs, w_ref, v_ref, 0.1, 0.9, 0.001)
+    torch.cuda.synchronize()
+    for r in range(N):
+        compare(from_dev(w_d[r]), w_ref, "f32", what=f"graph bucket set w N={N} r{r}")
+    gdraa.gdraa_vr_bucket_set_begin_streamed(N, 8)   # (its device state exists before
+    gdraa.gdraa_vr_bucket_set_end(N, stream=s)         #  the capture below)
+    s.synchronize()
+    with pytest.raises(gdraa.GdraaError) as e:
+        with torch.cuda.graph(torch.cuda.CUDAGraph(), stream=s):
+            gdraa.gdraa_vr_bucket_set_begin_streamed(N, 8)
+            try:
+                gdraa.gdraa_vr_sgd_step_range(w_d, g_d, v_d, 0, 1024, 0.1, 0.9, 0.0, stream=s)
+            finally:
+                gdraa.gdraa_vr_bucket_set_end(N, stream=s)
+    assert e.value.name == "GDRAA_EINVAL" and "captured" in str(e.value)
+
+
 # ---------------------------------------------------------------------------------------
 # NEXT-1: weight decay and the mixed-precision (bf16 model copy) all-gather.
 # ---------------------------------------------------------------------------------------
