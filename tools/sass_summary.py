@@ -5,7 +5,7 @@ instruction classes that back the DESIGN.md claims (128-bit peer loads / stores,
 copies + mbarriers, system fences, the FP ops of the fold / update, and where the FFMA
 come from), and saves a short excerpt of the inner loop.
 
-    python tools/sass_summary.py [out_prefix]     # default profiles/r62_sass
+    python tools/sass_summary.py [out_prefix]     # e.g. profiles/r98_sass
 """
 import collections
 import json
@@ -19,20 +19,24 @@ SO = os.path.join(ROOT, "paper_1802_02326_b200", "lib", "libgdraa.so")
 
 # (label, mangled-name regex): the kernels bench.py's configs and the small-message path run
 DEFAULT_PATH = [
-    ("N=1 local fused SGD, fp32 (gdraa_kernel<float,1,kSgd,U1,512,2>)",
-     r"12gdraa_kernelIfLi1ELi1ELi1ELi512ELi2EEE"),
+    ("N=1 local fused SGD, fp32 (gdraa_kernel<float,1,kSgd,U4,512,1>)",
+     r"12gdraa_kernelIfLi1ELi1ELi4ELi512ELi1EEE"),
     ("N=2 two-shot fused SGD, fp32, TMA-staged (gdraa_tma_kernel<float,2,kSgd>)",
-     r"16gdraa_tma_kernelIfLi2ELi1ELi16ELi4ELi4ELi4ELi0E(Li0E)?EE"),
+     r"16gdraa_tma_kernelIfLi2ELi1ELi16ELi4ELi4ELi4ELi0ELi0ELi40EEE"),
     ("N=4 two-shot fused SGD, fp32, TMA-staged (gdraa_tma_kernel<float,4,kSgd>)",
-     r"16gdraa_tma_kernelIfLi4ELi1ELi16ELi4ELi4ELi4ELi0E(Li0E)?EE"),
+     r"16gdraa_tma_kernelIfLi4ELi1ELi16ELi4ELi4ELi4ELi0ELi0ELi40EEE"),
+    ("N=2 two-shot fused SGD, bf16 g, TMA-staged (gdraa_tma_kernel<bf16,2,kSgd>)",
+     r"16gdraa_tma_kernelI13__nv_bfloat16Li2ELi1ELi16ELi4ELi4ELi4ELi0ELi0ELi40EEE"),
     ("N=4 two-shot mixed-precision SGD, bf16 g (gdraa_tma_kernel<bf16,4,kSgdMp>)",
-     r"16gdraa_tma_kernelI13__nv_bfloat16Li4ELi2ELi16ELi4ELi4ELi4ELi0E(Li0E)?EE"),
-    ("N=2 two-shot fused SGD, bf16 g, LSU (gdraa_kernel<bf16,2,kSgd,U2,1024,1>)",
-     r"12gdraa_kernelI13__nv_bfloat16Li2ELi1ELi2ELi1024ELi1EEE"),
+     r"16gdraa_tma_kernelI13__nv_bfloat16Li4ELi2ELi16ELi4ELi4ELi4ELi0ELi0ELi40EEE"),
     ("N=2 small-message SGD, fp32 (gdraa_ll_sgd_kernel<float,2,kSgd>)",
      r"19gdraa_ll_sgd_kernelIfLi2ELi1EEE"),
     ("N=2 small-message mean, fp32 (gdraa_ll_kernel<float,2>)",
      r"15gdraa_ll_kernelIfLi2EEE"),
+    ("N=2 streamed bucket set, fp32 sgd (gdraa_tma_set_kernel<float,2,kSgd>)",
+     r"20gdraa_tma_set_kernelIfLi2ELi1EEE"),
+    ("bucket-set exit barrier (gdraa_exit_kernel)",
+     r"17gdraa_exit_kernel"),
 ]
 
 CLASSES = {
