@@ -702,3 +702,24 @@ def test_multiprocess_world8_oversubscribed(tmp_path):
     reps = [json.load(open(tmp_path / f"w8_{r}.json")) for r in range(world)]
     assert line["ok"] and line["data_bytes"] == 0 and line["ranks_joined"] == 8, line
     assert line["done"] == [reps[0]["calls"]] * world, line
+
+
+def test_soak_short(tmp_path):
+    """tools/soak.py for 15 s: random calls of every entry point (sets, streamed sets, two
+    streams, both size classes) through the multi-process path, each checked bit for bit
+    (time-sliced ranks on a one-GPU box)."""
+    import socket
+    import subprocess
+    import sys
+    world = mp_world()
+    with socket.socket() as t:
+        t.bind(("127.0.0.1", 0))
+        port = t.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.join(root, "tools", "soak.py"), "--seconds", "15", "--max-elems", "1000000"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["iterations"] > 0 and d["mismatches"] == 0, d

@@ -38,10 +38,17 @@ def main():
     world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
     local = int(os.environ["LOCAL_RANK"])
     assert world & (world - 1) == 0, "world must be a power of two (exact integer family)"
+    # ranks share GPUs (time-sliced) when there are fewer GPUs than ranks: gloo plumbing
+    shared = torch.cuda.device_count() < world
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
-    js = jobserver.setup_for_rank(world, rank, local, tag="soak" + os.environ["MASTER_PORT"])
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+    js = jobserver.setup_for_rank(world, rank, int(os.environ["LOCAL_RANK"]),
+                                  tag="soak" + os.environ["MASTER_PORT"])
     gdraa.gdraa_init(world, rank)
 
     M = args.max_elems
@@ -68,7 +75,7 @@ def main():
     t_end = time.time() + args.seconds
     it = 0
     while True:
-        stop = torch.tensor([1 if time.time() > t_end else 0], device=dev)
+        stop = torch.tensor([1 if time.time() > t_end else 0], device="cpu" if shared else dev)
         dist.all_reduce(stop, op=dist.ReduceOp.MAX)   # every rank stops at the same call
         if stop.item():
             break
